@@ -1,0 +1,160 @@
+/*
+ * lfprobe_b200.h -- C ABI of the B200 probe-grid tracer (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   render_frame(ProbeGrid, Camera)          pkg/src/lfprobe/render.py:102-153
+ *     -> kernels.render_grid(...)            pkg/src/lfprobe/kernels.py:825-843
+ *        -> trace_grid_ray(...)              pkg/src/lfprobe/kernels.py:653-822
+ * The reference crosses Python -> numba native code exactly once, at
+ * render.py:132-136; these entry points are what that call site binds to
+ * instead (see INTEGRATION.md for the ctypes binding).
+ *
+ * Conventions
+ *  - plain C types only; every pointer is caller-owned unless stated;
+ *  - array layouts are the reference's (C-contiguous, [ty][tx] texels);
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *  - every call returns LFP_OK (0) or a negative error code and never
+ *    throws; lfp_last_error() returns a thread-local message;
+ *  - probe sets are immutable after creation and may be used by concurrent
+ *    renders on different streams / host threads (the reference kernel is
+ *    pure over immutable inputs and is called concurrently by the service,
+ *    service.py:136, 189).
+ */
+#ifndef LFPROBE_B200_H
+#define LFPROBE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFP_OK 0
+#define LFP_ERR_INVALID -1   /* bad argument (shape, null pointer, dims) */
+#define LFP_ERR_CUDA -2      /* CUDA runtime error                       */
+#define LFP_ERR_NOMEM -3     /* device allocation failed                 */
+
+/* status codes, kernels.py:18-20 */
+#define LFP_MISS 0
+#define LFP_HIT 1
+#define LFP_UNKNOWN 2
+
+/* lfp_probeset_create flags */
+#define LFP_SRC_DEVICE 0x1u     /* source pointers are device pointers       */
+#define LFP_FMT_AUTO_HALF 0x2u  /* store dir/irr as half4 when lossless      */
+#define LFP_FMT_FORCE_F32 0x4u  /* never compress payloads                   */
+
+typedef struct lfp_probeset lfp_probeset;
+
+/* Trace parameters: grid geometry (grid.py:48-93) + TraceConfig
+ * (trace.py:32-40). */
+typedef struct {
+    double grid_origin[3];
+    double cell;            /* scalar cubic cell (grid.py:51-57)          */
+    int32_t nx, ny, nz;     /* probe counts per axis                      */
+    double eps_start;       /* default 1e-4 (kernels.py:25)               */
+    double eps_align;       /* default 1e-4 (kernels.py:27)               */
+    double slack;           /* default 1e-3 (kernels.py:23)               */
+} lfp_grid_params;
+
+/* Pinhole camera (render.py:24-62). `basis` = (right, up, forward) exactly
+ * as Camera.basis() returns them; tan_v = tan(radians(vfov)/2),
+ * tan_h = tan_v * width / height, all computed on the host. */
+typedef struct {
+    double eye[3];
+    double basis[9];
+    double tan_v, tan_h;
+} lfp_camera;
+
+/* Per-ray outputs; any pointer may be NULL to skip that output.
+ *  status u8[n]      MISS / HIT / UNKNOWN (grid mode never yields UNKNOWN)
+ *  rgb    f32[n*3]   see rgb_mode
+ *  probe  i32[n]     hit probe, or last-UNKNOWN probe diagnostic, or -1
+ *  texel  i32[n]     tx | (ty << 16) of that probe texel, or -1
+ *  fetch  i32[n]     reference-equivalent texel fetch count (K:216,341,443,628)
+ *  hit_t  f32[n]     HIT: (origin_p + dist_hi[p,ty,tx] * v_texel - eye) . d,
+ *                    else +inf (SURVEY.md §8(c) hit-distance definition)
+ *  stats  u64[4]     accumulated: {sum fetch, #MISS, #UNKNOWN, #HIT}
+ * rgb_mode 0 = frame fill (render.py:147-149): HIT radiance, MISS
+ * `background`, UNKNOWN `unknown_color`; rgb_mode 1 = kernel semantics
+ * (kernels.py:840-843): only HIT rows are written. */
+typedef struct {
+    uint8_t* status;
+    float* rgb;
+    int32_t* probe;
+    int32_t* texel;
+    int32_t* fetch;
+    float* hit_t;
+    unsigned long long* stats;
+    int32_t rgb_mode;
+    float background[3];
+    float unknown_color[3];
+} lfp_outputs;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int lfp_version(void);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* lfp_last_error(void);
+
+/* Upload + relayout a ProbeSet (grid.py:19-45 arrays):
+ *   dist_hi f32[P][R][R], dir_hi f32[P][R][R][3], irr_hi f32[P][R][R][3],
+ *   dist_lo f32[P][r][r], origins f64[P][3]
+ * into device-resident tracing layouts on `device` (pre-dilated low-res
+ * MIN, float4/half4 payloads, texel-centre direction table). Replaces the
+ * per-call array hand-off of render.py:132-136 / grid.py:76-80. */
+int lfp_probeset_create(int device, const float* dist_hi, const float* dir_hi,
+                        const float* irr_hi, const float* dist_lo,
+                        const double* origins, int64_t P, int32_t R,
+                        int32_t r, uint32_t flags, void* stream,
+                        lfp_probeset** out);
+
+int lfp_probeset_destroy(lfp_probeset* ps);
+
+/* Device bytes held by the probe set, and which payload formats it chose. */
+int lfp_probeset_info(const lfp_probeset* ps, int64_t* device_bytes,
+                      int32_t* dir_half, int32_t* irr_half);
+
+/* render_frame(ProbeGrid, Camera) for a batch of cameras sharing one
+ * resolution (render.py:102-153; ray generation render.py:50-62 fused in).
+ * The frame is cut into 8x16-pixel tiles numbered camera-major, row-major;
+ * this call traces tiles tile_begin, tile_begin + tile_step, ... (n_tiles of
+ * them). compact == 0: outputs are indexed like the frames,
+ * cam * H * W + y * W + x (arrays sized n_cams * H * W). compact == 1:
+ * outputs are indexed local_tile * 128 + (y % 16) * 8 + (x % 8) (arrays
+ * sized n_tiles * 128; pixels past the frame edge are left untouched) --
+ * the per-GPU shard layout gathered by lfp_untile. */
+int lfp_render_cameras(const lfp_probeset* ps, const lfp_grid_params* grid,
+                       const lfp_camera* cams_host, int32_t n_cams,
+                       int32_t width, int32_t height, int64_t tile_begin,
+                       int64_t tile_step, int64_t n_tiles, int32_t compact,
+                       const lfp_outputs* out, void* stream);
+
+/* Number of 8x16 tiles of a batch of n_cams frames of width x height. */
+int64_t lfp_num_tiles(int32_t n_cams, int32_t width, int32_t height);
+
+/* kernels.render_grid (kernels.py:825-843): one shared eye, explicit unit
+ * directions dirs[n][3] (device, f64 if dirs_f32 == 0 else f32). */
+int lfp_render_grid(const lfp_probeset* ps, const lfp_grid_params* grid,
+                    const double* eye, const void* dirs, int32_t dirs_f32,
+                    int64_t n, const lfp_outputs* out, void* stream);
+
+/* trace_grid_ray (kernels.py:653-822) over n explicit rays with per-ray
+ * origins (device arrays [n][3], f64 if f32 == 0 else f32 up-cast
+ * exactly). Config 5 and the parity harness. */
+int lfp_trace_rays(const lfp_probeset* ps, const lfp_grid_params* grid,
+                   const void* ray_origins, const void* ray_dirs, int32_t f32,
+                   int64_t n, const lfp_outputs* out, void* stream);
+
+/* Scatter compact-tile outputs of `n_ranks` shards (rank-major
+ * concatenation, shard k traced tiles k, k + n_ranks, ...) back into frame
+ * order. Any of the array pairs may be NULL. */
+int lfp_untile(int32_t n_cams, int32_t width, int32_t height, int32_t n_ranks,
+               const uint8_t* status_in, const float* rgb_in,
+               uint8_t* status_out, float* rgb_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFPROBE_B200_H */

@@ -1,0 +1,153 @@
+"""Seeded benchmark configurations C1..C5 (BASELINE.json `configs`,
+SURVEY.md §8(d)). Every seed is fixed here; scenes, probes, cameras and
+incoherent rays are synthetic stand-ins built from these seeds.
+
+  C1  room 4x4 floor, 3 m high, 8 boxes + 4 spheres; 2x2x2 probes, cell 4,
+      32^2 / 8^2 f32 maps; one 128x128 view, 60 deg
+  C2  same generator, new seed; 4x4x4 probes, cell 4/3, 128^2 / 32^2 f32;
+      one 512x512 view
+  C3  room 7x7 floor, 3 m high, 64 boxes + 32 spheres; 8x4x8 probes, cell 1,
+      256^2 / 64^2, f32 distance, fp16 radiance / direction; 64 poses at
+      1920x1080
+  C5  the C3 probe set; 2^26 rays, origins U(room interior), directions
+      normalised Gaussian, stored f32 and up-cast exactly on both sides
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .bake import bake_grid
+from .grid import ProbeGrid, ProbeSet
+from .render import Camera
+from .scenes import free_point, room_scene
+
+
+@dataclass
+class Config:
+    name: str
+    scene: object
+    grid: ProbeGrid
+    cameras: list
+    description: str
+
+    @property
+    def rays_per_batch(self):
+        return sum(c.width * c.height for c in self.cameras)
+
+
+def random_cameras(scene, n, width, height, seed, vfov=60.0,
+                   pitch_deg=30.0, margin=0.3):
+    """Eye ~ U(interior, >= margin from walls, outside primitives); forward
+    ~ U(yaw) with pitch U[-pitch, pitch]."""
+    rng = np.random.default_rng(seed)
+    cams = []
+    for _ in range(n):
+        eye = free_point(scene, rng, margin=margin)
+        yaw = rng.uniform(0.0, 2.0 * np.pi)
+        pitch = np.radians(rng.uniform(-pitch_deg, pitch_deg))
+        fwd = (np.cos(pitch) * np.cos(yaw), np.sin(pitch),
+               np.cos(pitch) * np.sin(yaw))
+        cams.append(Camera(eye=tuple(float(v) for v in eye),
+                           forward=tuple(float(v) for v in fwd),
+                           vfov_deg=vfov, width=width, height=height))
+    return cams
+
+
+def _cache_dir():
+    d = os.environ.get("LFP_CACHE_DIR",
+                       os.path.join(os.path.expanduser("~"), ".cache",
+                                    "lfprobe_b200"))
+    os.makedirs(d, exist_ok=True)
+    return d
+
+
+def _cached_bake(key, fn):
+    """Memoise a deterministic bake on disk (pure speed-up: the content is a
+    function of `key`; a missing or stale file is simply rebaked)."""
+    path = os.path.join(_cache_dir(), hashlib.sha1(key.encode()).hexdigest()
+                        + ".npz")
+    if os.path.exists(path):
+        try:
+            z = np.load(path)
+            return ProbeSet(arrays=(z["dist_hi"], z["dir_hi"], z["irr_hi"],
+                                    z["dist_lo"], z["origins"]))
+        except Exception:
+            pass
+    ps = fn()
+    tmp = path + f".{os.getpid()}.tmp.npz"
+    np.savez(tmp, dist_hi=ps.dist_hi, dir_hi=ps.dir_hi, irr_hi=ps.irr_hi,
+             dist_lo=ps.dist_lo, origins=ps.origins)
+    os.replace(tmp, path)
+    return ps
+
+
+def c1(seed=101, cam_seed=1101, width=128, height=128):
+    scene = room_scene(seed, size=(4.0, 3.0, 4.0), n_boxes=8, n_spheres=4)
+    grid = bake_grid(scene, (0.0, 0.0, 0.0), 4.0, (2, 2, 2), 32, 8)
+    cams = random_cameras(scene, 1, width, height, cam_seed)
+    return Config("c1", scene, grid, cams,
+                  "room 4x4x3 m, 8 boxes + 4 spheres; 2x2x2 probes cell 4; "
+                  "32^2/8^2 f32; 128x128 view")
+
+
+def c2(seed=202, cam_seed=2202, width=512, height=512, n_views=1):
+    scene = room_scene(seed, size=(4.0, 3.0, 4.0), n_boxes=8, n_spheres=4)
+    grid = bake_grid(scene, (0.0, 0.0, 0.0), 4.0 / 3.0, (4, 4, 4), 128, 32)
+    cams = random_cameras(scene, n_views, width, height, cam_seed)
+    return Config("c2", scene, grid, cams,
+                  "room 4x4x3 m, 8 boxes + 4 spheres; 4x4x4 probes cell 4/3; "
+                  "128^2/32^2 f32; 512x512 view")
+
+
+def c3_scene(seed=303):
+    return room_scene(seed, size=(7.0, 3.0, 7.0), n_boxes=64, n_spheres=32,
+                      box_side=(0.2, 1.0), sphere_r=(0.1, 0.5))
+
+
+def c3_grid(seed=303, use_cache=True):
+    scene = c3_scene(seed)
+    dims = (8, 4, 8)
+
+    def bake():
+        return bake_grid(scene, (0.0, 0.0, 0.0), 1.0, dims, 256, 64,
+                         quant="f16").probe_set
+
+    ps = _cached_bake(f"c3-v1-{seed}", bake) if use_cache else bake()
+    return scene, ProbeGrid((0.0, 0.0, 0.0), 1.0, dims, probe_set=ps)
+
+
+def c3(seed=303, cam_seed=3303, n_views=64, width=1920, height=1080,
+       use_cache=True):
+    scene, grid = c3_grid(seed, use_cache)
+    cams = random_cameras(scene, n_views, width, height, cam_seed)
+    return Config("c3", scene, grid, cams,
+                  "room 7x7x3 m, 64 boxes + 32 spheres; 8x4x8 probes cell 1; "
+                  "256^2/64^2 f32 dist, f16 radiance/direction; "
+                  f"{n_views} poses at {width}x{height}")
+
+
+def c5_rays(scene, n, seed=505):
+    """Incoherent rays: origins U(interior), directions normalised Gaussian
+    (`pkg/tests/conftest.py:29-31`), both stored as float32."""
+    rng = np.random.default_rng(seed)
+    lo = np.asarray(scene.interior_lo, np.float64)
+    hi = np.asarray(scene.interior_hi, np.float64)
+    o = rng.uniform(lo, hi, size=(n, 3)).astype(np.float32)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    return o, d.astype(np.float32)
+
+
+def probe_set_digest(ps):
+    h = hashlib.sha256()
+    for a in (ps.dist_hi, ps.dir_hi, ps.irr_hi, ps.dist_lo, ps.origins):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+BUILDERS = {"c1": c1, "c2": c2, "c3": c3}

@@ -1,0 +1,226 @@
+"""Device-resident probe sets and the launch wrappers around the C ABI.
+
+torch provides device memory, streams and events (plumbing); all compute
+runs in liblfprobe_b200.so. Nothing here falls back to the CPU: a missing
+library or GPU raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+
+import numpy as np
+import torch
+
+from . import native
+from .trace import DEFAULT_CONFIG
+
+_TILE = 128   # pixels per 8x16 tile (lfp_render_cameras)
+
+
+def _require_cuda(device):
+    if not torch.cuda.is_available():
+        raise native.LfpError("no CUDA device: the B200 tracer has no CPU path")
+    return torch.device("cuda", device if isinstance(device, int) else
+                        torch.device(device).index or 0)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class DeviceProbeSet:
+    """Immutable device copy of a ProbeSet (`lfp_probeset_create`)."""
+
+    def __init__(self, dist_hi, dir_hi, irr_hi, dist_lo, origins, device=0,
+                 half="auto", stream=None):
+        self.device = _require_cuda(device)
+        arrs = [np.ascontiguousarray(dist_hi, np.float32),
+                np.ascontiguousarray(dir_hi, np.float32),
+                np.ascontiguousarray(irr_hi, np.float32),
+                np.ascontiguousarray(dist_lo, np.float32),
+                np.ascontiguousarray(origins, np.float64)]
+        P, R, R2 = arrs[0].shape
+        r = arrs[3].shape[1]
+        if R != R2 or arrs[1].shape != (P, R, R, 3) or arrs[2].shape != (
+                P, R, R, 3) or arrs[3].shape != (P, r, r) or arrs[4].shape != (P, 3):
+            raise ValueError("probe set arrays have inconsistent shapes")
+        flags = {"auto": native.LFP_FMT_AUTO_HALF, "never": native.LFP_FMT_FORCE_F32
+                 }[half]
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            st = stream if stream is not None else torch.cuda.current_stream(self.device)
+            native.check(native.lib().lfp_probeset_create(
+                self.device.index, *[a.ctypes.data_as(ctypes.c_void_p) for a in arrs],
+                P, R, r, flags, ctypes.c_void_p(st.cuda_stream),
+                ctypes.byref(handle)))
+        self.handle = handle
+        self.P, self.R, self.r = P, R, r
+        self._fin = weakref.finalize(self, native.lib().lfp_probeset_destroy,
+                                     handle)
+
+    @classmethod
+    def from_probe_set(cls, ps, device=0, half="auto"):
+        return cls(ps.dist_hi, ps.dir_hi, ps.irr_hi, ps.dist_lo, ps.origins,
+                   device=device, half=half)
+
+    def info(self):
+        b = ctypes.c_int64()
+        dh = ctypes.c_int32()
+        ih = ctypes.c_int32()
+        native.check(native.lib().lfp_probeset_info(self.handle, ctypes.byref(b),
+                                                    ctypes.byref(dh),
+                                                    ctypes.byref(ih)))
+        return {"device_bytes": b.value, "dir_half": bool(dh.value),
+                "irr_half": bool(ih.value)}
+
+    def close(self):
+        self._fin()
+
+
+def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG):
+    g = native.GridParams()
+    for k in range(3):
+        g.grid_origin[k] = float(grid_origin[k])
+    g.cell = float(cell)
+    g.nx, g.ny, g.nz = (int(d) for d in dims)
+    g.eps_start = float(config.eps_start)
+    g.eps_align = float(config.eps_align)
+    g.slack = float(config.slack)
+    return g
+
+
+def camera_struct(cam):
+    """Host-side camera parameters computed with the same numpy calls as
+    Camera.basis / Camera.ray_directions (render.py:33-55)."""
+    r, u, f = cam.basis()
+    tan_v = np.tan(np.radians(cam.vfov_deg) / 2.0)
+    tan_h = tan_v * cam.width / cam.height
+    c = native.CameraC()
+    eye = np.asarray(cam.eye, dtype=np.float64)
+    for k in range(3):
+        c.eye[k] = float(eye[k])
+        c.basis[k] = float(r[k])
+        c.basis[3 + k] = float(u[k])
+        c.basis[6 + k] = float(f[k])
+    c.tan_v = float(tan_v)
+    c.tan_h = float(tan_h)
+    return c
+
+
+class RayOutputs:
+    """Device output buffers for n rays (torch tensors)."""
+
+    def __init__(self, n, device, status=True, rgb=True, probe=False,
+                 texel=False, fetch=False, hit_t=False, stats=True):
+        kw = dict(device=device)
+        self.n = n
+        self.status = torch.empty(n, dtype=torch.uint8, **kw) if status else None
+        self.rgb = torch.empty((n, 3), dtype=torch.float32, **kw) if rgb else None
+        self.probe = torch.empty(n, dtype=torch.int32, **kw) if probe else None
+        self.texel = torch.empty(n, dtype=torch.int32, **kw) if texel else None
+        self.fetch = torch.empty(n, dtype=torch.int32, **kw) if fetch else None
+        self.hit_t = torch.empty(n, dtype=torch.float32, **kw) if hit_t else None
+        self.stats = torch.zeros(4, dtype=torch.int64, **kw) if stats else None
+
+    def struct(self, rgb_mode=0, background=(0.0, 0.0, 0.0),
+               unknown_color=(1.0, 0.0, 1.0)):
+        o = native.Outputs()
+        o.status = _ptr(self.status)
+        o.rgb = _ptr(self.rgb)
+        o.probe = _ptr(self.probe)
+        o.texel = _ptr(self.texel)
+        o.fetch = _ptr(self.fetch)
+        o.hit_t = _ptr(self.hit_t)
+        o.stats = _ptr(self.stats)
+        o.rgb_mode = int(rgb_mode)
+        for k in range(3):
+            o.background[k] = float(background[k])
+            o.unknown_color[k] = float(unknown_color[k])
+        return o
+
+
+def num_tiles(n_cams, width, height):
+    return int(native.lib().lfp_num_tiles(n_cams, width, height))
+
+
+def render_cameras(dps, gparams, cams, width, height, out, tile_begin=0,
+                   tile_step=1, n_tiles=None, compact=False, rgb_mode=0,
+                   background=(0.0, 0.0, 0.0), unknown_color=(1.0, 0.0, 1.0),
+                   stream=None):
+    """Launch lfp_render_cameras on `stream` (default: current stream)."""
+    cams_c = (native.CameraC * len(cams))(*[camera_struct(c) for c in cams])
+    total = num_tiles(len(cams), width, height)
+    if n_tiles is None:
+        n_tiles = (total - tile_begin + tile_step - 1) // tile_step
+    st = stream if stream is not None else torch.cuda.current_stream(dps.device)
+    o = out.struct(rgb_mode, background, unknown_color)
+    native.check(native.lib().lfp_render_cameras(
+        dps.handle, ctypes.byref(gparams), cams_c, len(cams), width, height,
+        tile_begin, tile_step, n_tiles, int(compact), ctypes.byref(o),
+        ctypes.c_void_p(st.cuda_stream)))
+    return n_tiles
+
+
+def trace_rays(dps, gparams, origins, dirs, out, rgb_mode=1, stream=None):
+    """lfp_trace_rays: origins/dirs are device tensors (N, 3), both f64 or
+    both f32."""
+    if origins.dtype != dirs.dtype or dirs.dtype not in (torch.float32,
+                                                         torch.float64):
+        raise ValueError("origins and dirs must share dtype f32 or f64")
+    origins = origins.contiguous()
+    dirs = dirs.contiguous()
+    st = stream if stream is not None else torch.cuda.current_stream(dps.device)
+    o = out.struct(rgb_mode)
+    native.check(native.lib().lfp_trace_rays(
+        dps.handle, ctypes.byref(gparams), _ptr(origins), _ptr(dirs),
+        int(dirs.dtype == torch.float32), dirs.shape[0], ctypes.byref(o),
+        ctypes.c_void_p(st.cuda_stream)))
+
+
+def render_grid_dirs(dps, gparams, eye, dirs, out, rgb_mode=1, stream=None):
+    """lfp_render_grid: shared eye, device dirs (N, 3) f64/f32."""
+    dirs = dirs.contiguous()
+    e = (ctypes.c_double * 3)(*[float(v) for v in eye])
+    st = stream if stream is not None else torch.cuda.current_stream(dps.device)
+    o = out.struct(rgb_mode)
+    native.check(native.lib().lfp_render_grid(
+        dps.handle, ctypes.byref(gparams), e, _ptr(dirs),
+        int(dirs.dtype == torch.float32), dirs.shape[0], ctypes.byref(o),
+        ctypes.c_void_p(st.cuda_stream)))
+
+
+def untile(n_cams, width, height, n_ranks, status_in, rgb_in, status_out,
+           rgb_out, stream=None):
+    st = stream if stream is not None else torch.cuda.current_stream()
+    native.check(native.lib().lfp_untile(
+        n_cams, width, height, n_ranks, _ptr(status_in), _ptr(rgb_in),
+        _ptr(status_out), _ptr(rgb_out), ctypes.c_void_p(st.cuda_stream)))
+
+
+# ---- probe-set cache: one device copy per (host arrays, device) ----------
+
+_CACHE = {}
+
+
+def cached_probe_set(dist_hi, dir_hi, irr_hi, dist_lo, origins, device=0):
+    """Device probe set for these exact host arrays (identity-keyed, like
+    the reference's cached ProbeSet, grid.py:76-80). The arrays are treated
+    as immutable, as the reference does."""
+    arrs = (dist_hi, dir_hi, irr_hi, dist_lo, origins)
+    key = tuple(id(a) for a in arrs) + (int(device),)
+    hit = _CACHE.get(key)
+    if hit is not None:
+        refs, dps = hit
+        if all(r() is a for r, a in zip(refs, arrs)):
+            return dps
+    dps = DeviceProbeSet(*arrs, device=device)
+    try:
+        refs = tuple(weakref.ref(a) for a in arrs)
+    except TypeError:
+        return dps
+    _CACHE[key] = (refs, dps)
+    for r in refs:   # drop the entry when any source array dies
+        weakref.finalize(r(), _CACHE.pop, key, None)
+    return dps
