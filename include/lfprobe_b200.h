@@ -146,12 +146,15 @@ int lfp_trace_rays(const lfp_probeset* ps, const lfp_grid_params* grid,
                    const void* ray_origins, const void* ray_dirs, int32_t f32,
                    int64_t n, const lfp_outputs* out, void* stream);
 
-/* Scatter compact-tile outputs of `n_ranks` shards (rank-major
- * concatenation, shard k traced tiles k, k + n_ranks, ...) back into frame
- * order. Any of the array pairs may be NULL. */
+/* Scatter compact-tile outputs of `n_ranks` shards back into frame order.
+ * Shard k traced tiles k, k + n_ranks, ...; its j-th tile sits at tile slot
+ * k * shard_stride + j of the input (shard_stride = 0: shards packed
+ * back to back, shard k holding floor(T/n) + (k < T % n) tiles). Any of the
+ * array pairs may be NULL. */
 int lfp_untile(int32_t n_cams, int32_t width, int32_t height, int32_t n_ranks,
-               const uint8_t* status_in, const float* rgb_in,
-               uint8_t* status_out, float* rgb_out, void* stream);
+               int64_t shard_stride, const uint8_t* status_in,
+               const float* rgb_in, uint8_t* status_out, float* rgb_out,
+               void* stream);
 
 #ifdef __cplusplus
 }

@@ -192,10 +192,11 @@ def render_grid_dirs(dps, gparams, eye, dirs, out, rgb_mode=1, stream=None):
 
 
 def untile(n_cams, width, height, n_ranks, status_in, rgb_in, status_out,
-           rgb_out, stream=None):
+           rgb_out, shard_stride=0, stream=None):
     st = stream if stream is not None else torch.cuda.current_stream()
     native.check(native.lib().lfp_untile(
-        n_cams, width, height, n_ranks, _ptr(status_in), _ptr(rgb_in),
+        n_cams, width, height, n_ranks, int(shard_stride), _ptr(status_in),
+        _ptr(rgb_in),
         _ptr(status_out), _ptr(rgb_out), ctypes.c_void_p(st.cuda_stream)))
 
 

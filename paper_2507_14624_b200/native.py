@@ -82,7 +82,7 @@ def lib():
         L.lfp_trace_rays.argtypes = [
             vp, ctypes.POINTER(GridParams), vp, vp, i32, i64,
             ctypes.POINTER(Outputs), vp]
-        L.lfp_untile.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp]
+        L.lfp_untile.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
         for name in ("lfp_probeset_create", "lfp_probeset_destroy",
                      "lfp_probeset_info", "lfp_render_cameras",
                      "lfp_render_grid", "lfp_trace_rays", "lfp_untile"):
