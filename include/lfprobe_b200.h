@@ -156,6 +156,36 @@ int lfp_untile(int32_t n_cams, int32_t width, int32_t height, int32_t n_ranks,
                const float* rgb_in, uint8_t* status_out, float* rgb_out,
                void* stream);
 
+/* ---- input production: GPU ray-cast bake ---- */
+
+/* Analytic primitive: kind 0 = axis-aligned box (a = lo, b = hi), kind 1 =
+ * sphere (a = centre, b[0] = radius). */
+typedef struct {
+    int32_t kind;
+    double a[3];
+    double b[3];
+    float albedo[3];
+} lfp_prim;
+
+typedef struct {
+    double position[3];
+    double power;     /* falloff min(1, power / (1 + d^2)) */
+    double ambient;
+} lfp_light;
+
+/* Bake P probes (origins_host f64[P][3]) of R x R texels by ray-casting the
+ * texel-centre directions against the primitives; writes the reference
+ * ProbeSet layout into caller-owned DEVICE arrays dist_hi f32[P][R][R],
+ * dir_hi / irr_hi f32[P][R][R][3], dist_lo f32[P][r][r] (block MIN,
+ * bake.py:94-102). quant_f16 rounds radiance / direction through half.
+ * Synchronous on `stream`. Replaces the point-cloud bake of bake.py:140-207
+ * for the analytic benchmark scenes. */
+int lfp_bake_probes(int device, const lfp_prim* prims_host, int32_t n_prims,
+                    const lfp_light* light, const double* origins_host,
+                    int64_t P, int32_t R, int32_t r, int32_t quant_f16,
+                    int32_t shadows, float* dist_hi, float* dir_hi,
+                    float* irr_hi, float* dist_lo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,73 @@ def bake_probes(scene, origins, r_hi, r_lo, quant="f32", shadows=True,
                             origins))
 
 
+def scene_prims(scene):
+    """Scene primitives / light as the C structs of lfp_bake_probes."""
+    from . import native
+    from .scenes import Box
+    prims = (native.PrimC * len(scene.primitives))()
+    for i, p in enumerate(scene.primitives):
+        if isinstance(p, Box):
+            prims[i].kind = 0
+            a, b = p.lo, p.hi
+        else:
+            prims[i].kind = 1
+            a, b = p.center, (p.radius, 0.0, 0.0)
+        for k in range(3):
+            prims[i].a[k] = float(a[k])
+            prims[i].b[k] = float(b[k])
+            prims[i].albedo[k] = float(p.albedo[k])
+    light = native.LightC()
+    for k in range(3):
+        light.position[k] = float(scene.light.position[k])
+    light.power = float(scene.light.power)
+    light.ambient = float(scene.light.ambient)
+    return prims, light
+
+
+def bake_probes_gpu(scene, origins, r_hi, r_lo, quant="f32", shadows=True,
+                    device=0, keep_device=False):
+    """GPU ray-cast bake (`lfp_bake_probes`); returns a host ProbeSet (and
+    the device tensors when keep_device)."""
+    import ctypes
+
+    import torch
+
+    from . import native
+    if r_hi % r_lo != 0:
+        raise ValueError("r_hi must be a multiple of r_lo")
+    if not torch.cuda.is_available():
+        raise native.LfpError("GPU bake needs a CUDA device")
+    origins = np.ascontiguousarray(np.asarray(origins, np.float64).reshape(-1, 3))
+    P = len(origins)
+    dv = torch.device("cuda", device)
+    t_dist = torch.empty((P, r_hi, r_hi), dtype=torch.float32, device=dv)
+    t_dir = torch.empty((P, r_hi, r_hi, 3), dtype=torch.float32, device=dv)
+    t_irr = torch.empty((P, r_hi, r_hi, 3), dtype=torch.float32, device=dv)
+    t_lo = torch.empty((P, r_lo, r_lo), dtype=torch.float32, device=dv)
+    prims, light = scene_prims(scene)
+    st = torch.cuda.current_stream(dv)
+    vp = ctypes.c_void_p
+    native.check(native.lib().lfp_bake_probes(
+        device, prims, len(scene.primitives), ctypes.byref(light),
+        origins.ctypes.data_as(vp), P, r_hi, r_lo, int(quant == "f16"),
+        int(bool(shadows)), vp(t_dist.data_ptr()), vp(t_dir.data_ptr()),
+        vp(t_irr.data_ptr()), vp(t_lo.data_ptr()), vp(st.cuda_stream)))
+    ps = ProbeSet(arrays=(t_dist.cpu().numpy(), t_dir.cpu().numpy(),
+                          t_irr.cpu().numpy(), t_lo.cpu().numpy(), origins))
+    if keep_device:
+        return ps, (t_dist, t_dir, t_irr, t_lo)
+    return ps
+
+
+def bake_grid_gpu(scene, grid_origin, cell, dims, r_hi, r_lo, quant="f32",
+                  shadows=True, device=0):
+    ps = bake_probes_gpu(scene, lattice_origins(grid_origin, cell, dims),
+                         r_hi, r_lo, quant=quant, shadows=shadows,
+                         device=device)
+    return ProbeGrid(grid_origin, cell, dims, probe_set=ps)
+
+
 def lattice_origins(grid_origin, cell, dims):
     nx, ny, nz = dims
     ii, jj, kk = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz),

@@ -16,13 +16,12 @@ incoherent rays are synthetic stand-ins built from these seeds.
 from __future__ import annotations
 
 import hashlib
-import os
 from dataclasses import dataclass
 
 import numpy as np
 
-from .bake import bake_grid
-from .grid import ProbeGrid, ProbeSet
+from .bake import bake_grid, bake_grid_gpu
+from .grid import ProbeGrid
 from .render import Camera
 from .scenes import free_point, room_scene
 
@@ -58,34 +57,6 @@ def random_cameras(scene, n, width, height, seed, vfov=60.0,
     return cams
 
 
-def _cache_dir():
-    d = os.environ.get("LFP_CACHE_DIR",
-                       os.path.join(os.path.expanduser("~"), ".cache",
-                                    "lfprobe_b200"))
-    os.makedirs(d, exist_ok=True)
-    return d
-
-
-def _cached_bake(key, fn):
-    """Memoise a deterministic bake on disk (pure speed-up: the content is a
-    function of `key`; a missing or stale file is simply rebaked)."""
-    path = os.path.join(_cache_dir(), hashlib.sha1(key.encode()).hexdigest()
-                        + ".npz")
-    if os.path.exists(path):
-        try:
-            z = np.load(path)
-            return ProbeSet(arrays=(z["dist_hi"], z["dir_hi"], z["irr_hi"],
-                                    z["dist_lo"], z["origins"]))
-        except Exception:
-            pass
-    ps = fn()
-    tmp = path + f".{os.getpid()}.tmp.npz"
-    np.savez(tmp, dist_hi=ps.dist_hi, dir_hi=ps.dir_hi, irr_hi=ps.irr_hi,
-             dist_lo=ps.dist_lo, origins=ps.origins)
-    os.replace(tmp, path)
-    return ps
-
-
 def c1(seed=101, cam_seed=1101, width=128, height=128):
     scene = room_scene(seed, size=(4.0, 3.0, 4.0), n_boxes=8, n_spheres=4)
     grid = bake_grid(scene, (0.0, 0.0, 0.0), 4.0, (2, 2, 2), 32, 8)
@@ -109,21 +80,18 @@ def c3_scene(seed=303):
                       box_side=(0.2, 1.0), sphere_r=(0.1, 0.5))
 
 
-def c3_grid(seed=303, use_cache=True):
+def c3_grid(seed=303, device=0):
+    """C3 probes, baked on the GPU (lfp_bake_probes): 256 probes x 256^2
+    texels ray-cast against 102 primitives with shadow rays."""
     scene = c3_scene(seed)
-    dims = (8, 4, 8)
-
-    def bake():
-        return bake_grid(scene, (0.0, 0.0, 0.0), 1.0, dims, 256, 64,
-                         quant="f16").probe_set
-
-    ps = _cached_bake(f"c3-v1-{seed}", bake) if use_cache else bake()
-    return scene, ProbeGrid((0.0, 0.0, 0.0), 1.0, dims, probe_set=ps)
+    grid = bake_grid_gpu(scene, (0.0, 0.0, 0.0), 1.0, (8, 4, 8), 256, 64,
+                         quant="f16", device=device)
+    return scene, grid
 
 
 def c3(seed=303, cam_seed=3303, n_views=64, width=1920, height=1080,
-       use_cache=True):
-    scene, grid = c3_grid(seed, use_cache)
+       device=0):
+    scene, grid = c3_grid(seed, device)
     cams = random_cameras(scene, n_views, width, height, cam_seed)
     return Config("c3", scene, grid, cams,
                   "room 7x7x3 m, 64 boxes + 32 spheres; 8x4x8 probes cell 1; "

@@ -38,6 +38,16 @@ class CameraC(ctypes.Structure):
                 ("tan_v", ctypes.c_double), ("tan_h", ctypes.c_double)]
 
 
+class PrimC(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("a", ctypes.c_double * 3),
+                ("b", ctypes.c_double * 3), ("albedo", ctypes.c_float * 3)]
+
+
+class LightC(ctypes.Structure):
+    _fields_ = [("position", ctypes.c_double * 3), ("power", ctypes.c_double),
+                ("ambient", ctypes.c_double)]
+
+
 class Outputs(ctypes.Structure):
     _fields_ = [("status", ctypes.c_void_p), ("rgb", ctypes.c_void_p),
                 ("probe", ctypes.c_void_p), ("texel", ctypes.c_void_p),
@@ -83,7 +93,10 @@ def lib():
             vp, ctypes.POINTER(GridParams), vp, vp, i32, i64,
             ctypes.POINTER(Outputs), vp]
         L.lfp_untile.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
-        for name in ("lfp_probeset_create", "lfp_probeset_destroy",
+        L.lfp_bake_probes.argtypes = [
+            ctypes.c_int, ctypes.POINTER(PrimC), i32, ctypes.POINTER(LightC),
+            vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+        for name in ("lfp_bake_probes", "lfp_probeset_create", "lfp_probeset_destroy",
                      "lfp_probeset_info", "lfp_render_cameras",
                      "lfp_render_grid", "lfp_trace_rays", "lfp_untile"):
             getattr(L, name).restype = ctypes.c_int
@@ -102,4 +115,4 @@ def exported_symbols():
     return ["lfp_version", "lfp_last_error", "lfp_probeset_create",
             "lfp_probeset_destroy", "lfp_probeset_info", "lfp_render_cameras",
             "lfp_num_tiles", "lfp_render_grid", "lfp_trace_rays",
-            "lfp_untile"]
+            "lfp_untile", "lfp_bake_probes"]
