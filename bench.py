@@ -257,7 +257,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--mode", default="filtered",
+                    choices=["filtered", "exact", "check"],
+                    help="trace_mode: fp32 decision filters + exact fallback "
+                         "(default), exact fp64 only, or self-check")
+    ap.add_argument("--lib", default=None,
+                    help="alternative liblfprobe_b200 build (LFP_LIB_PATH)")
     args = ap.parse_args()
+    if args.lib:
+        os.environ["LFP_LIB_PATH"] = os.path.abspath(args.lib)
     args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
@@ -285,7 +293,7 @@ def main():
     W, H = cams[0].width, cams[0].height
     dps = device_probe_set(cfg.grid, local)
     g = dev.grid_params(cfg.grid.grid_origin, cfg.grid.cell_size, cfg.grid.dims,
-                        DEFAULT_CONFIG)
+                        DEFAULT_CONFIG, mode=args.mode)
     plan = pdist.ShardPlan(len(cams), W, H, world, rank)
     stream = torch.cuda.current_stream()
     dvc = torch.device("cuda", local)
@@ -424,6 +432,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
+            "trace_mode": args.mode,
+            "lib": os.path.basename(os.environ.get("LFP_LIB_PATH", "")) or
+                   "liblfprobe_b200.so",
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -55,6 +55,11 @@ typedef struct {
     double eps_start;       /* default 1e-4 (kernels.py:25)               */
     double eps_align;       /* default 1e-4 (kernels.py:27)               */
     double slack;           /* default 1e-3 (kernels.py:23)               */
+    int32_t trace_mode;     /* 0 = filtered (default): fp32 decision filters
+                               with exact fp64 fallback, outputs identical to
+                               the reference; 1 = exact fp64 on every step;
+                               2 = filtered + re-check of every filtered
+                               decision (counts into lfp_outputs.diag)    */
 } lfp_grid_params;
 
 /* Pinhole camera (render.py:24-62). `basis` = (right, up, forward) exactly
@@ -86,6 +91,9 @@ typedef struct {
     int32_t* fetch;
     float* hit_t;
     unsigned long long* stats;
+    unsigned long long* diag;   /* u64[5]: low-res decisions taken by the
+                                   filter / by the exact path, hi-res ditto,
+                                   filter-vs-exact disagreements (mode 2)  */
     int32_t rgb_mode;
     float background[3];
     float unknown_color[3];

@@ -79,7 +79,11 @@ class DeviceProbeSet:
         self._fin()
 
 
-def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG):
+TRACE_MODES = {"filtered": 0, "exact": 1, "check": 2}
+
+
+def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG,
+                mode="filtered"):
     g = native.GridParams()
     for k in range(3):
         g.grid_origin[k] = float(grid_origin[k])
@@ -88,6 +92,7 @@ def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG):
     g.eps_start = float(config.eps_start)
     g.eps_align = float(config.eps_align)
     g.slack = float(config.slack)
+    g.trace_mode = TRACE_MODES[mode]
     return g
 
 
@@ -113,7 +118,8 @@ class RayOutputs:
     """Device output buffers for n rays (torch tensors)."""
 
     def __init__(self, n, device, status=True, rgb=True, probe=False,
-                 texel=False, fetch=False, hit_t=False, stats=True):
+                 texel=False, fetch=False, hit_t=False, stats=True,
+                 diag=False):
         kw = dict(device=device)
         self.n = n
         self.status = torch.empty(n, dtype=torch.uint8, **kw) if status else None
@@ -123,6 +129,7 @@ class RayOutputs:
         self.fetch = torch.empty(n, dtype=torch.int32, **kw) if fetch else None
         self.hit_t = torch.empty(n, dtype=torch.float32, **kw) if hit_t else None
         self.stats = torch.zeros(4, dtype=torch.int64, **kw) if stats else None
+        self.diag = torch.zeros(5, dtype=torch.int64, **kw) if diag else None
 
     def struct(self, rgb_mode=0, background=(0.0, 0.0, 0.0),
                unknown_color=(1.0, 0.0, 1.0)):
@@ -134,6 +141,7 @@ class RayOutputs:
         o.fetch = _ptr(self.fetch)
         o.hit_t = _ptr(self.hit_t)
         o.stats = _ptr(self.stats)
+        o.diag = _ptr(self.diag)
         o.rgb_mode = int(rgb_mode)
         for k in range(3):
             o.background[k] = float(background[k])

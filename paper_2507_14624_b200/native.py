@@ -11,7 +11,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblfprobe_b200.so")
+# LFP_LIB_PATH selects an alternative build (tools/build_variants.py)
+LIB_PATH = os.environ.get("LFP_LIB_PATH") or os.path.join(_HERE,
+                                                          "liblfprobe_b200.so")
 
 LFP_SRC_DEVICE = 0x1
 LFP_FMT_AUTO_HALF = 0x2
@@ -29,7 +31,8 @@ class GridParams(ctypes.Structure):
                 ("nz", ctypes.c_int32),
                 ("eps_start", ctypes.c_double),
                 ("eps_align", ctypes.c_double),
-                ("slack", ctypes.c_double)]
+                ("slack", ctypes.c_double),
+                ("trace_mode", ctypes.c_int32)]
 
 
 class CameraC(ctypes.Structure):
@@ -53,6 +56,7 @@ class Outputs(ctypes.Structure):
                 ("probe", ctypes.c_void_p), ("texel", ctypes.c_void_p),
                 ("fetch", ctypes.c_void_p), ("hit_t", ctypes.c_void_p),
                 ("stats", ctypes.c_void_p),
+                ("diag", ctypes.c_void_p),
                 ("rgb_mode", ctypes.c_int32),
                 ("background", ctypes.c_float * 3),
                 ("unknown_color", ctypes.c_float * 3)]

@@ -362,3 +362,60 @@ class TestGpuBake:
         np.testing.assert_array_equal(
             np.isfinite(b.dist_lo),
             np.isfinite(b.dist_hi.reshape(8, 8, 4, 8, 4)).any(axis=(2, 4)))
+
+
+class TestDecisionFilters:
+    """The fp32 decision filters never change a decision: every filtered
+    decision is re-checked against the exact fp64 path (trace_mode
+    'check') and the filtered, exact and check modes produce identical
+    outputs."""
+
+    def _run(self, grid, o, d, mode):
+        dev = _dev()
+        from paper_2507_14624_b200.render import device_probe_set
+        from paper_2507_14624_b200.trace import DEFAULT_CONFIG
+        dps = device_probe_set(grid)
+        g = dev.grid_params(grid.grid_origin, grid.cell_size, grid.dims,
+                            DEFAULT_CONFIG, mode=mode)
+        dt = torch.float32 if d.dtype == np.float32 else torch.float64
+        n = len(d)
+        o = np.broadcast_to(np.asarray(o), (n, 3))
+        out = dev.RayOutputs(n, dps.device, probe=True, texel=True, fetch=True,
+                             diag=True)
+        dev.trace_rays(dps, g, torch.as_tensor(np.ascontiguousarray(o), dtype=dt).cuda(),
+                       torch.as_tensor(np.ascontiguousarray(d), dtype=dt).cuda(),
+                       out, rgb_mode=1)
+        torch.cuda.synchronize()
+        return {k: getattr(out, k).cpu().numpy() for k in
+                ("status", "probe", "texel", "fetch", "diag")}
+
+    def _check(self, grid, o, d):
+        a = self._run(grid, o, d, "exact")
+        b = self._run(grid, o, d, "filtered")
+        c = self._run(grid, o, d, "check")
+        for k in ("status", "probe", "texel", "fetch"):
+            np.testing.assert_array_equal(a[k], b[k])
+            np.testing.assert_array_equal(a[k], c[k])
+        lo_fast, lo_slow, hi_fast, hi_slow, mism = (int(v) for v in c["diag"])
+        assert mism == 0, f"{mism} filtered decisions disagree with exact fp64"
+        assert lo_fast + lo_slow > 0 and hi_fast + hi_slow > 0
+        # the filter must decide the bulk of the steps
+        assert lo_fast / (lo_fast + lo_slow) > 0.9
+        assert hi_fast / (hi_fast + hi_slow) > 0.8
+        return c["diag"]
+
+    def test_c2_frame(self):
+        from paper_2507_14624_b200 import configs
+        cfg = configs.c2()
+        cam = cfg.cameras[0]
+        self._check(cfg.grid, np.asarray(cam.eye), cam.ray_directions())
+
+    def test_pcgrid_incoherent(self, golden):
+        z = golden("pcgrid")
+        self._check(golden_grid(z), z["inc_origins"], z["inc_dirs"])
+
+    def test_c5_incoherent(self):
+        from paper_2507_14624_b200 import configs
+        scene, grid = configs.c3_grid()
+        o32, d32 = configs.c5_rays(scene, 1 << 18, seed=515)
+        self._check(grid, o32, d32)

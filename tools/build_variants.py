@@ -1,0 +1,19 @@
+"""Build register-budget variants of the CUDA library into build/variants/
+(select one at run time with LFP_LIB_PATH=...)."""
+import os
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import __graft_entry__ as g  # noqa: E402
+
+out = os.path.join(REPO, "build", "variants")
+os.makedirs(out, exist_ok=True)
+srcs = [os.path.join(g.CSRC, "lfp_capi.cu"), os.path.join(g.CSRC, "lfp_bake.cu")]
+for mb in sys.argv[1:] or ["1", "2", "3", "4", "5"]:
+    lib = os.path.join(out, f"liblfprobe_b200_mb{mb}.so")
+    subprocess.run([g._nvcc(), *g.NVCC_FLAGS, f"-DLFP_MIN_BLOCKS={mb}",
+                    "-Xptxas", "-v", "-o", lib, *srcs], check=True,
+                   stderr=open(lib + ".ptxas.txt", "w"))
+    print(lib)
