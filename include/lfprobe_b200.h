@@ -141,6 +141,28 @@ int lfp_render_cameras(const lfp_probeset* ps, const lfp_grid_params* grid,
                        int64_t tile_step, int64_t n_tiles, int32_t compact,
                        const lfp_outputs* out, void* stream);
 
+/* render_frame for the non-grid sources (render.py:118-144), same camera
+ * batching, frame-ordered outputs:
+ *  LFP_SOURCE_SINGLE  one probe, full marching over the padded bounds
+ *                     (render_single_probe, kernels.py:567-596)
+ *  LFP_SOURCE_FEW     a probe list in nearest-first `order` (stable by
+ *                     squared eye distance, computed by the caller) with
+ *                     MISS/UNKNOWN fall-through over the padded union bounds
+ *                     (render_few_probes, kernels.py:846-892; returns UNKNOWN)
+ *  LFP_SOURCE_LOOKUP  eye at the probe: one octahedral lookup per pixel
+ *                     (_lookup_render, render.py:86-99)
+ * The probe set holds 1 probe for SINGLE / LOOKUP. Only eps_start,
+ * eps_align, slack and trace_mode of `params` are used. */
+#define LFP_SOURCE_SINGLE 1
+#define LFP_SOURCE_FEW 2
+#define LFP_SOURCE_LOOKUP 3
+int lfp_render_probes(const lfp_probeset* ps, int32_t source_kind,
+                      const int32_t* order, int32_t n_order,
+                      const double* bounds_lo, const double* bounds_hi,
+                      const lfp_grid_params* params, const lfp_camera* cams_host,
+                      int32_t n_cams, int32_t width, int32_t height,
+                      const lfp_outputs* out, void* stream);
+
 /* Number of 8x16 tiles of a batch of n_cams frames of width x height. */
 int64_t lfp_num_tiles(int32_t n_cams, int32_t width, int32_t height);
 

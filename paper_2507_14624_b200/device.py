@@ -171,6 +171,29 @@ def render_cameras(dps, gparams, cams, width, height, out, tile_begin=0,
     return n_tiles
 
 
+def render_probes(dps, kind, cams, width, height, out, gparams, order=None,
+                  bounds=None, background=(0.0, 0.0, 0.0),
+                  unknown_color=(1.0, 0.0, 1.0), stream=None):
+    """lfp_render_probes: single-probe / few-probe / eye-aligned lookup
+    render of a camera batch (frame-ordered outputs)."""
+    cams_c = (native.CameraC * len(cams))(*[camera_struct(c) for c in cams])
+    n_order = 0
+    order_c = None
+    if order is not None:
+        n_order = len(order)
+        order_c = (ctypes.c_int32 * n_order)(*[int(v) for v in order])
+    lo = hi = None
+    if bounds is not None:
+        lo = (ctypes.c_double * 3)(*[float(v) for v in bounds[0]])
+        hi = (ctypes.c_double * 3)(*[float(v) for v in bounds[1]])
+    st = stream if stream is not None else torch.cuda.current_stream(dps.device)
+    o = out.struct(0, background, unknown_color)
+    native.check(native.lib().lfp_render_probes(
+        dps.handle, int(kind), order_c, n_order, lo, hi, ctypes.byref(gparams),
+        cams_c, len(cams), width, height, ctypes.byref(o),
+        ctypes.c_void_p(st.cuda_stream)))
+
+
 def trace_rays(dps, gparams, origins, dirs, out, rgb_mode=1, stream=None):
     """lfp_trace_rays: origins/dirs are device tensors (N, 3), both f64 or
     both f32."""
@@ -218,18 +241,24 @@ def cached_probe_set(dist_hi, dir_hi, irr_hi, dist_lo, origins, device=0):
     the reference's cached ProbeSet, grid.py:76-80). The arrays are treated
     as immutable, as the reference does."""
     arrs = (dist_hi, dir_hi, irr_hi, dist_lo, origins)
-    key = tuple(id(a) for a in arrs) + (int(device),)
+    return cached_for(arrs, lambda: arrs, device)
+
+
+def cached_for(key_objs, arrays_fn, device=0):
+    """Device probe set cached on the identity of `key_objs` (weakly held);
+    `arrays_fn()` yields the five host arrays on a miss."""
+    key = tuple(id(a) for a in key_objs) + (int(device),)
     hit = _CACHE.get(key)
     if hit is not None:
         refs, dps = hit
-        if all(r() is a for r, a in zip(refs, arrs)):
+        if all(r() is a for r, a in zip(refs, key_objs)):
             return dps
-    dps = DeviceProbeSet(*arrs, device=device)
+    dps = DeviceProbeSet(*arrays_fn(), device=device)
     try:
-        refs = tuple(weakref.ref(a) for a in arrs)
+        refs = tuple(weakref.ref(a) for a in key_objs)
     except TypeError:
         return dps
     _CACHE[key] = (refs, dps)
-    for r in refs:   # drop the entry when any source array dies
+    for r in refs:   # drop the entry when any key object dies
         weakref.finalize(r(), _CACHE.pop, key, None)
     return dps

@@ -19,6 +19,10 @@ LFP_SRC_DEVICE = 0x1
 LFP_FMT_AUTO_HALF = 0x2
 LFP_FMT_FORCE_F32 = 0x4
 
+LFP_SOURCE_SINGLE = 1
+LFP_SOURCE_FEW = 2
+LFP_SOURCE_LOOKUP = 3
+
 
 class LfpError(RuntimeError):
     pass
@@ -88,6 +92,10 @@ def lib():
         L.lfp_render_cameras.argtypes = [
             vp, ctypes.POINTER(GridParams), ctypes.POINTER(CameraC), i32, i32,
             i32, i64, i64, i64, i32, ctypes.POINTER(Outputs), vp]
+        L.lfp_render_probes.argtypes = [
+            vp, i32, ctypes.POINTER(i32), i32, ctypes.POINTER(ctypes.c_double),
+            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(GridParams),
+            ctypes.POINTER(CameraC), i32, i32, i32, ctypes.POINTER(Outputs), vp]
         L.lfp_num_tiles.argtypes = [i32, i32, i32]
         L.lfp_num_tiles.restype = i64
         L.lfp_render_grid.argtypes = [
@@ -100,7 +108,8 @@ def lib():
         L.lfp_bake_probes.argtypes = [
             ctypes.c_int, ctypes.POINTER(PrimC), i32, ctypes.POINTER(LightC),
             vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-        for name in ("lfp_bake_probes", "lfp_probeset_create", "lfp_probeset_destroy",
+        for name in ("lfp_bake_probes", "lfp_render_probes",
+                     "lfp_probeset_create", "lfp_probeset_destroy",
                      "lfp_probeset_info", "lfp_render_cameras",
                      "lfp_render_grid", "lfp_trace_rays", "lfp_untile"):
             getattr(L, name).restype = ctypes.c_int
@@ -119,4 +128,4 @@ def exported_symbols():
     return ["lfp_version", "lfp_last_error", "lfp_probeset_create",
             "lfp_probeset_destroy", "lfp_probeset_info", "lfp_render_cameras",
             "lfp_num_tiles", "lfp_render_grid", "lfp_trace_rays",
-            "lfp_untile", "lfp_bake_probes"]
+            "lfp_untile", "lfp_bake_probes", "lfp_render_probes"]

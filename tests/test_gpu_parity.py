@@ -419,3 +419,37 @@ class TestDecisionFilters:
         scene, grid = configs.c3_grid()
         o32, d32 = configs.c5_rays(scene, 1 << 18, seed=515)
         self._check(grid, o32, d32)
+
+
+class TestNonGridSources:
+    """render_frame on a ProbeData (single-probe marching K:567-596 and the
+    eye-aligned lookup R:86-99) and on a probe list (K:846-892) vs the
+    reference's own frames (tests/golden/modes.npz)."""
+
+    def _probe(self, z, i):
+        from paper_2507_14624_b200 import MapChain, ProbeData
+        ch = MapChain(irradiance_hi=z[f"p{i}_irr_hi"],
+                      distance_hi=z[f"p{i}_dist_hi"],
+                      direction_hi=z[f"p{i}_dir_hi"],
+                      distance_lo=z[f"p{i}_dist_lo"])
+        return ProbeData(origin=z[f"p{i}_origin"], chain=ch,
+                         bounds_lo=z[f"p{i}_blo"], bounds_hi=z[f"p{i}_bhi"])
+
+    @pytest.mark.parametrize("name", ["single", "few", "lookup"])
+    def test_vs_reference(self, golden, name):
+        from paper_2507_14624_b200 import render_frame
+        z = golden("modes")
+        probes = [self._probe(z, i) for i in range(3)]
+        src = {"single": probes[0], "few": probes, "lookup": probes[1]}[name]
+        cam = golden_camera(z, name + "_")
+        fr = render_frame(src, cam)
+        np.testing.assert_array_equal(fr.status, z[name + "_frame_status"])
+        np.testing.assert_array_equal(fr.pixels, z[name + "_frame_pixels"])
+        assert fr.stats["perPixelTexelFetches"] == pytest.approx(
+            float(z[name + "_frame_fetch_mean"]), abs=1e-12)
+        assert fr.stats["unknownFraction"] == pytest.approx(
+            float(z[name + "_frame_unknown"]), abs=1e-12)
+        if name == "lookup":
+            assert fr.stats["perPixelTexelFetches"] == 1.0
+        else:
+            assert fr.stats["unknownFraction"] > 0.1   # UNKNOWN -> magenta

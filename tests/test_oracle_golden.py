@@ -150,3 +150,58 @@ def test_c2_full_frame(golden):
     _check_outputs(res, z, "cam_")
     pix, st = oracle.frame_pixels(res, cam.height, cam.width)
     np.testing.assert_array_equal(pix, z["cam_frame_pixels"])
+
+
+class TestNonGridModes:
+    """render_frame's single-probe / probe-list / eye-aligned sources
+    (render.py:118-144) restated by the oracle vs the reference's frames."""
+
+    def _probe(self, z, i):
+        return {k: z[f"p{i}_{k}"] for k in ("dist_hi", "dir_hi", "irr_hi",
+                                           "dist_lo", "origin", "blo", "bhi")}
+
+    def _fill(self, st, rgb):
+        px = rgb.astype(np.float32)
+        px[st == 0] = 0.0
+        px[st == 2] = np.array([1.0, 0.0, 1.0], np.float32)
+        return px
+
+    def test_single_probe(self, golden):
+        z = golden("modes")
+        p = self._probe(z, 0)
+        cam = golden_camera(z, "single_")
+        st, rgb, fe = oracle.render_single_probe(
+            p["dist_hi"], p["dir_hi"], p["irr_hi"], p["dist_lo"], p["origin"],
+            np.asarray(cam.eye, np.float64), z["single_dirs"], p["blo"] - 0.5,
+            p["bhi"] + 0.5, 1e-4, 1e-3)
+        np.testing.assert_array_equal(st.reshape(cam.height, cam.width),
+                                      z["single_frame_status"])
+        np.testing.assert_array_equal(
+            self._fill(st, rgb).reshape(cam.height, cam.width, 3),
+            z["single_frame_pixels"])
+        assert fe.mean() == z["single_frame_fetch_mean"]
+        assert (st == 2).mean() == z["single_frame_unknown"] > 0.1
+
+    def test_probe_list(self, golden):
+        from types import SimpleNamespace
+        z = golden("modes")
+        ps = [self._probe(z, i) for i in range(3)]
+        cam = golden_camera(z, "few_")
+        eye = np.asarray(cam.eye, np.float64)
+        stack = SimpleNamespace(
+            dist_hi=np.stack([p["dist_hi"] for p in ps]),
+            dir_hi=np.stack([p["dir_hi"] for p in ps]),
+            irr_hi=np.stack([p["irr_hi"] for p in ps]),
+            dist_lo=np.stack([p["dist_lo"] for p in ps]),
+            origins=np.stack([p["origin"] for p in ps]))
+        blo = np.min([p["blo"] for p in ps], axis=0) - 0.5
+        bhi = np.max([p["bhi"] for p in ps], axis=0) + 0.5
+        st, rgb, fe = oracle.render_few_probes(stack, blo, bhi, eye,
+                                               z["few_dirs"], 1e-4, 1e-4, 1e-3)
+        np.testing.assert_array_equal(st.reshape(cam.height, cam.width),
+                                      z["few_frame_status"])
+        np.testing.assert_array_equal(
+            self._fill(st, rgb).reshape(cam.height, cam.width, 3),
+            z["few_frame_pixels"])
+        assert fe.mean() == z["few_frame_fetch_mean"]
+        assert (st == 2).any()
