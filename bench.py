@@ -1,18 +1,25 @@
 """Benchmark: probe-traced Mrays/s (and frames/s) of the B200 grid tracer.
 
-    python bench.py [--gpus N --steps K --warmup W --config c2|c1|c3]
+    python bench.py [--gpus N --steps K --warmup W --config c2|c1|c3|c5]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # CPU reference arm (oracle port)
 
-A step renders one batch of synthetic frames with the config's probe grid.
-Weak scaling: every rank owns a fixed share (one config batch) of a global
-batch of N config batches; the global batch's 8x16 tiles are interleaved
-over the ranks, each rank traces its tiles against its own probe-set replica
-and rank 0 gathers the framebuffer over NCCL (the only collective) and
-untiles it. Inputs (probe set, camera parameters) are resident before the
-timed region; L2 (126 MB) is flushed between steps by writing 512 MiB
-outside the timed events, since the C2 probe set (28 MB) would otherwise
-stay L2-resident across steps.
+Workloads (BASELINE.json configs, seeded synthetic inputs, configs.py):
+  c2 (default) 4x4x4 probes 128^2/32^2, one 512x512 view per GPU per step.
+     Weak scaling: the global batch has N views; its 8x16 pixel tiles are
+     interleaved over the ranks, each rank traces its tiles against its own
+     probe-set replica, rank 0 gathers the framebuffer over NCCL (the only
+     collective) and untiles it.
+  c1 the same with the 2x2x2 / 32^2 room and a 128x128 view.
+  c3 8x4x8 probes 256^2/64^2 (fp16 payloads), 64 poses at 1920x1080 per
+     step, tiles interleaved over the N ranks (strong scaling).
+  c5 the c3 probe set, 2^26 incoherent f32 rays per step split into N
+     contiguous batches (strong scaling); each rank bins its rays by
+     (entry cube, direction octant), sorts and traces them in bin order,
+     rank 0 gathers the per-ray results.
+Inputs (probe set, cameras / rays) are resident in HBM before the timed
+region. L2 (126 MB) is flushed between steps by a 512 MiB write outside the
+timed events (the c2 probe set, 28 MB, would otherwise stay L2-resident).
 """
 
 from __future__ import annotations
@@ -33,6 +40,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "probe-traced Mrays/s and frames/s at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "Mrays/s"
+C5_RAYS = 1 << 26
 
 _REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting",
             0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x10: "sync_boost",
@@ -77,6 +85,7 @@ class ClockSampler:
                     self.rows.append(parts)
         self.thread = threading.Thread(target=read, daemon=True)
         self.thread.start()
+        time.sleep(0.15)
         return self
 
     def __exit__(self, *exc):
@@ -91,11 +100,12 @@ class ClockSampler:
                 self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         for r in self.rows:
             try:
                 sm.append(float(r[0]))
                 mx.append(float(r[1]))
+                pw.append(float(r[2]))
                 mask = int(r[3], 16)
             except ValueError:
                 continue
@@ -107,6 +117,7 @@ class ClockSampler:
                     "samples": 0}
         loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx),
+                "power_w_max": max(pw) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -125,52 +136,61 @@ def build_config(name, views):
         return configs.c1()
     if name == "c2":
         return configs.c2(n_views=views)
-    if name == "c3":
+    if name in ("c3", "c5"):
         return configs.c3(n_views=views)
     raise SystemExit(f"unknown config {name}")
 
 
-def config_views(name):
-    return {"c1": 1, "c2": 1, "c3": 64}[name]
-
-
-def config_record(cfg, name, world, per_rank_views):
-    cam = cfg.cameras[0]
+def config_record(cfg, name, world, views):
     ps = cfg.grid.probe_set
-    return {
+    rec = {
         "workload": f"{name.upper()}: {cfg.description}",
         "probes": int(ps.dist_hi.shape[0]),
         "res_hi": int(ps.dist_hi.shape[1]), "res_lo": int(ps.dist_lo.shape[1]),
+        "l2": "flushed between steps (512 MiB write, outside timed events)",
+        "seeds": "configs.py (scene/bake/camera/ray seeds fixed)",
+    }
+    if name == "c5":
+        rec.update({"workload": "C5: incoherent-ray stress, 2^26 f32 rays "
+                                "(origins U(room), directions normalised "
+                                "Gaussian) against the C3 probe set",
+                    "rays_per_step": C5_RAYS,
+                    "parallelism": f"ray-batch sharded x{world}, per-rank "
+                                   "binning by (entry cube, octant)" +
+                                   (", NCCL gather to rank 0" if world > 1 else "")})
+        return rec
+    cam = cfg.cameras[0]
+    rec.update({
         "frame": [cam.width, cam.height],
-        "views_per_gpu": per_rank_views,
-        "global_views": per_rank_views * world,
-        "rays_per_step": per_rank_views * world * cam.width * cam.height,
+        "views_per_step": views,
+        "rays_per_step": views * cam.width * cam.height,
         "parallelism": f"tile-sharded x{world} (interleaved 8x16 tiles), "
                        "probe set replicated" + (", NCCL gather to rank 0"
                                                  if world > 1 else ""),
-        "l2": "flushed between steps (512 MiB write, outside timed events)",
-        "seeds": "configs.py (scene/bake/camera seeds fixed)",
-    }
+    })
+    return rec
 
 
 # --------------------------------------------------------------------------
 # CPU reference arm / baseline (the oracle port -- test infrastructure)
 # --------------------------------------------------------------------------
 
-def cpu_sample(cfg, stride):
-    """Seeded pixel subsample of the config's first view: every `stride`-th
-    ray of the frame (row-major), f64 directions computed as render.py does."""
+def cpu_sample(cfg, name, stride):
+    """Bounded sample of the workload: every `stride`-th ray of view 0 (or
+    of the C5 ray set), f64, directions computed exactly as render.py."""
     from oracle import oracle
+    if name == "c5":
+        from paper_2507_14624_b200 import configs
+        o, d = configs.c5_rays(cfg.scene, C5_RAYS // stride, seed=505)
+        return o.astype(np.float64), d.astype(np.float64)
     cam = cfg.cameras[0]
     basis, tv, th = oracle.camera_params(cam)
     dirs = oracle.camera_dirs(basis, tv, th, cam.width, cam.height)
     return np.asarray(cam.eye, np.float64), np.ascontiguousarray(dirs[::stride])
 
 
-def run_cpu(cfg, eye, dirs, threads=None):
+def run_cpu(cfg, eye, dirs):
     from oracle import oracle
-    if threads:
-        oracle.set_num_threads(threads)
     g = cfg.grid
     t0 = time.perf_counter()
     res = oracle.trace_rays(g.probe_set, g.grid_origin, g.cell_size, g.dims,
@@ -178,14 +198,19 @@ def run_cpu(cfg, eye, dirs, threads=None):
     return time.perf_counter() - t0, res
 
 
-def cpu_baseline(cfg, budget_s=12.0, stride=1):
+CPU_STRIDE = {"c1": 1, "c2": 1, "c3": 16, "c5": 256}
+REF_STRIDE = {"c1": 1, "c2": 4, "c3": 64, "c5": 512}
+
+
+def cpu_baseline(cfg, name, budget_s=12.0):
     """Oracle port on all host threads over repeated passes of a bounded
     sample, ~budget_s of CPU time."""
     from oracle import oracle
     threads = os.cpu_count() or 1
     oracle.set_num_threads(threads)
-    eye, dirs = cpu_sample(cfg, stride)
-    run_cpu(cfg, eye, dirs[:4096])   # warm (page-in, thread pool)
+    stride = CPU_STRIDE[name]
+    eye, dirs = cpu_sample(cfg, name, stride)
+    run_cpu(cfg, eye if eye.ndim == 1 else eye[:4096], dirs[:4096])  # warm
     total_t, total_n, reps = 0.0, 0, 0
     while total_t < budget_s or reps == 0:
         dt, _ = run_cpu(cfg, eye, dirs)
@@ -196,7 +221,8 @@ def cpu_baseline(cfg, budget_s=12.0, stride=1):
             break
     return {"value": total_n / total_t / 1e6, "unit": UNIT, "cores": threads,
             "kind": "port",
-            "sample": f"{reps} pass(es) over every {stride}-th pixel of view 0 "
+            "sample": f"{reps} pass(es) over every {stride}-th ray of "
+                      f"{'the C5 ray set' if name == 'c5' else 'view 0'} "
                       f"({len(dirs)} rays/pass), C oracle (oracle/lfp_oracle.c"
                       f", OpenMP {threads} threads)"}
 
@@ -209,30 +235,32 @@ def run_reference(args):
     from oracle import oracle
     threads = os.cpu_count() or 1
     oracle.set_num_threads(threads)
-    stride = {"c1": 1, "c2": 4, "c3": 64}[args.config]
-    eye, dirs = cpu_sample(cfg, stride)
+    stride = REF_STRIDE[args.config]
+    eye, dirs = cpu_sample(cfg, args.config, stride)
     for _ in range(args.warmup):
         run_cpu(cfg, eye, dirs)
     times = []
+    res = None
     for _ in range(args.steps):
         dt, res = run_cpu(cfg, eye, dirs)
         times.append(dt)
     t = sum(times)
     value = len(dirs) * args.steps / t / 1e6
-    cam = cfg.cameras[0]
+    what = "the C5 ray set" if args.config == "c5" else "view 0"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if args.config in ("c1", "c2") else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded scene, ray-cast bake)",
         "config": config_record(cfg, args.config, 1, 1) | {
-            "reference_sample": f"every {stride}-th pixel of one "
-                                f"{cam.width}x{cam.height} view per step"},
+            "reference_sample": f"every {stride}-th ray of {what} per step "
+                                f"({len(dirs)} rays)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
                          "kind": "port",
                          "sample": f"{len(dirs)} rays per step (every "
-                                   f"{stride}-th pixel of view 0)"},
+                                   f"{stride}-th ray of {what})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "fetch_per_ray": float(res.fetch.mean()),
@@ -245,17 +273,204 @@ def run_reference(args):
 # GPU arm
 # --------------------------------------------------------------------------
 
+class Workload:
+    """One step of the hot path on this rank + its algorithmic bytes."""
+
+    def __init__(self, args, world, rank, dvc):
+        import torch
+
+        from paper_2507_14624_b200 import dist as pdist
+        from paper_2507_14624_b200 import device as dev
+        from paper_2507_14624_b200.render import device_probe_set
+        from paper_2507_14624_b200.trace import DEFAULT_CONFIG
+        self.torch, self.dev, self.pdist = torch, dev, pdist
+        self.name, self.world, self.rank, self.dvc = args.config, world, rank, dvc
+        self.gather_backend = args.dist_backend
+        name = args.config
+        if name in ("c1", "c2"):
+            self.views = args.views or 1
+            views_total = self.views * world          # weak scaling
+        elif name == "c3":
+            self.views = views_total = args.views or 64   # strong scaling
+        else:
+            self.views = views_total = 1
+        self.cfg = build_config(name, views_total)
+        self.dps = device_probe_set(self.cfg.grid, dvc.index)
+        self.g = dev.grid_params(self.cfg.grid.grid_origin,
+                                 self.cfg.grid.cell_size, self.cfg.grid.dims,
+                                 DEFAULT_CONFIG, mode=args.mode)
+        self.stream = torch.cuda.current_stream(dvc)
+        self.extra_in_bytes = 0
+        if name == "c5":
+            from paper_2507_14624_b200 import configs
+            lo = rank * C5_RAYS // world
+            hi = (rank + 1) * C5_RAYS // world
+            o, d = configs.c5_rays(self.cfg.scene, C5_RAYS, seed=505)
+            self.o = torch.from_numpy(o[lo:hi].copy()).to(dvc)
+            self.d = torch.from_numpy(d[lo:hi].copy()).to(dvc)
+            self.n_local = hi - lo
+            self.max_local = (C5_RAYS + world - 1) // world
+            self.out = dev.RayOutputs(self.max_local, dvc)
+            self.out.status.zero_()
+            self.out.rgb.zero_()
+            self.extra_in_bytes = 24
+            self.rays_per_step = C5_RAYS
+            self.frames_per_step = 0
+            self.binned = not args.no_binning
+        else:
+            cams = self.cfg.cameras
+            self.cams = cams
+            self.W, self.H = cams[0].width, cams[0].height
+            self.plan = pdist.ShardPlan(len(cams), self.W, self.H, world, rank)
+            n = len(cams) * self.W * self.H
+            if world == 1:
+                self.out = dev.RayOutputs(n, dvc)
+            else:
+                self.out = dev.RayOutputs(self.plan.max_tiles * pdist.TILE_PIX, dvc)
+                self.out.status.zero_()
+                self.out.rgb.zero_()
+            self.frame_st = self.frame_rgb = None
+            if world > 1 and rank == 0:
+                self.frame_st = torch.empty(n, dtype=torch.uint8, device=dvc)
+                self.frame_rgb = torch.empty((n, 3), dtype=torch.float32,
+                                             device=dvc)
+            self.rays_per_step = n
+            self.frames_per_step = len(cams)
+
+    # -- kernels -----------------------------------------------------------
+    def trace(self):
+        """The traced launch(es) of one step on this rank (no collective)."""
+        dev = self.dev
+        if self.name == "c5":
+            if self.binned:
+                keys = dev.bin_rays(self.g, self.o, self.d, stream=self.stream)
+                order = dev.ray_order(keys)
+                dev.trace_rays_ordered(self.dps, self.g, self.o, self.d, order,
+                                       self.out, stream=self.stream)
+            else:
+                dev.trace_rays(self.dps, self.g, self.o, self.d, self.out,
+                               stream=self.stream)
+            return
+        if self.world == 1:
+            dev.render_cameras(self.dps, self.g, self.cams, self.W, self.H,
+                               self.out, stream=self.stream)
+        else:
+            dev.render_cameras(self.dps, self.g, self.cams, self.W, self.H,
+                               self.out, tile_begin=self.plan.tile_begin,
+                               tile_step=self.plan.tile_step,
+                               n_tiles=self.plan.n_tiles, compact=True,
+                               stream=self.stream)
+
+    def gather(self):
+        """Framebuffer (or per-ray result) gather to rank 0 + untile."""
+        if self.world == 1:
+            return
+        torch, pdist = self.torch, self.pdist
+        st, rgb = self.out.status, self.out.rgb
+        if self.gather_backend == "gloo":
+            st, rgb = st.cpu(), rgb.cpu()
+        if self.name == "c5":
+            g = gather_padded(st, rgb, self.max_local)
+        else:
+            g = pdist.gather_shards(self.plan, st, rgb)
+        if g is None or self.name == "c5":
+            return
+        st_all, rgb_all = (t.to(self.dvc) for t in g)
+        self.dev.untile(len(self.cams), self.W, self.H, self.world, st_all,
+                        rgb_all, self.frame_st, self.frame_rgb,
+                        shard_stride=self.plan.max_tiles, stream=self.stream)
+
+    def launches_per_step(self):
+        if self.name == "c5":
+            # bin keys + sort (library) + ordered trace; only ours counted
+            return 2 if self.binned else 1
+        return 1 + (1 if (self.world > 1 and self.rank == 0) else 0)
+
+    def algorithmic_bytes(self):
+        """Sum of B_ray = 4 F + 12 H + 16 (+24 explicit ray input) over this
+        rank's rays of one launch."""
+        self.out.stats.zero_()
+        self.trace()
+        self.torch.cuda.synchronize()
+        f, m, u, h = (int(v) for v in self.out.stats.cpu())
+        n = m + u + h
+        return (4 * f + 12 * h + (16 + self.extra_in_bytes) * n, n, f, h)
+
+
+def gather_padded(st, rgb, m):
+    """Gather equal-size (padded) per-rank result buffers to rank 0."""
+    import torch
+    import torch.distributed as tdist
+    world = tdist.get_world_size()
+    if st.shape[0] < m:
+        st = torch.nn.functional.pad(st, (0, m - st.shape[0]))
+        rgb = torch.nn.functional.pad(rgb, (0, 0, 0, m - rgb.shape[0]))
+    if tdist.get_rank() == 0:
+        st_l = [torch.empty_like(st) for _ in range(world)]
+        rgb_l = [torch.empty_like(rgb) for _ in range(world)]
+    else:
+        st_l = rgb_l = None
+    tdist.gather(st, st_l, dst=0)
+    tdist.gather(rgb, rgb_l, dst=0)
+    if tdist.get_rank() == 0:
+        return torch.cat(st_l), torch.cat(rgb_l)
+    return None
+
+
+def e2e_measure(wl, steps, world, rank, local):
+    """Same metric through the public API with host buffers: render_frame
+    (camera configs) or trace_rays (C5) -- H2D of the step's inputs and
+    D2H of its results inside the timed region, per rank."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2507_14624_b200 as pkg
+    if wl.name == "c5":
+        n = min(wl.n_local, 1 << 22)
+        o_h = wl.o[:n].cpu().numpy()
+        d_h = wl.d[:n].cpu().numpy()
+        pkg.trace_rays(wl.cfg.grid, o_h, d_h, device=local)
+        call = lambda: pkg.trace_rays(wl.cfg.grid, o_h, d_h, device=local)  # noqa: E731
+        rays, h2d, d2h = n, 24 * n, 13 * n + 32
+        api = "trace_rays(ProbeGrid, origins, dirs) host f32 arrays -> host results"
+    else:
+        cam = wl.cams[rank % len(wl.cams)]
+        n = cam.width * cam.height
+        call = lambda: pkg.render_frame(wl.cfg.grid, cam, device=local)  # noqa: E731
+        call()
+        rays, h2d, d2h = n, 104, 13 * n + 32
+        api = "render_frame(ProbeGrid, Camera) -> Frame (host arrays)"
+    call()
+    k = max(3, min(steps, 20))
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        call()
+    dt = time.perf_counter() - t0
+    te = torch.tensor([dt], dtype=torch.float64, device=wl.dvc)
+    if world > 1 and wl.gather_backend == "nccl":
+        tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+    dt = float(te.item())
+    return {"value": world * k * rays / dt / 1e6, "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": api, "call_ms": dt / k * 1e3}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--views", type=int, default=0,
-                    help="views per GPU per step (default: the config's)")
+                    help="views per step (per GPU for c1/c2, total for c3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-binning", action="store_true",
+                    help="c5: trace rays in input order")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--mode", default="filtered",
                     choices=["filtered", "exact", "check"],
@@ -263,10 +478,13 @@ def main():
                          "(default), exact fp64 only, or self-check")
     ap.add_argument("--lib", default=None,
                     help="alternative liblfprobe_b200 build (LFP_LIB_PATH)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-logic test of the N>1 path on one GPU "
+                         "(gather through host memory)")
     args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
     if args.lib:
         os.environ["LFP_LIB_PATH"] = os.path.abspath(args.lib)
-    args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
         return run_reference(args)
@@ -274,65 +492,28 @@ def main():
     import torch
     import torch.distributed as tdist
 
-    from paper_2507_14624_b200 import device as dev
-    from paper_2507_14624_b200 import dist as pdist
-    from paper_2507_14624_b200 import render_frame
-    from paper_2507_14624_b200.render import device_probe_set
-    from paper_2507_14624_b200.trace import DEFAULT_CONFIG
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    views = args.views or config_views(args.config)
-    cfg = build_config(args.config, views * world)
-    cams = cfg.cameras
-    W, H = cams[0].width, cams[0].height
-    dps = device_probe_set(cfg.grid, local)
-    g = dev.grid_params(cfg.grid.grid_origin, cfg.grid.cell_size, cfg.grid.dims,
-                        DEFAULT_CONFIG, mode=args.mode)
-    plan = pdist.ShardPlan(len(cams), W, H, world, rank)
-    stream = torch.cuda.current_stream()
     dvc = torch.device("cuda", local)
-    if world == 1:
-        out = dev.RayOutputs(len(cams) * W * H, dvc)
-        frame_st = frame_rgb = None
-    else:
-        out = dev.RayOutputs(plan.max_tiles * pdist.TILE_PIX, dvc)
-        out.status.zero_()
-        out.rgb.zero_()
-        frame_st = torch.empty(len(cams) * W * H, dtype=torch.uint8,
-                               device=dvc) if rank == 0 else None
-        frame_rgb = torch.empty((len(cams) * W * H, 3), dtype=torch.float32,
-                                device=dvc) if rank == 0 else None
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dvc)
-    launches_per_step = 1 + (1 if (world > 1 and rank == 0) else 0)
-
-    def step():
-        if world == 1:
-            dev.render_cameras(dps, g, cams, W, H, out, stream=stream)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dvc)
         else:
-            pdist.render_batch_sharded(dps, g, cams, W, H, plan, out,
-                                       frame_st, frame_rgb, stream=stream)
+            tdist.init_process_group("gloo")
+
+    wl = Workload(args, world, rank, dvc)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dvc)
 
     for _ in range(args.warmup):
         flush.fill_(1.0)
-        step()
+        wl.trace()
+        wl.gather()
     torch.cuda.synchronize()
+    alg_bytes, n_local, fetch_sum, n_hit = wl.algorithmic_bytes()
 
-    # per-launch algorithmic bytes: B_ray = 4 F + 12 H + 16
-    out.stats.zero_()
-    dev.render_cameras(dps, g, cams, W, H, out, tile_begin=plan.tile_begin,
-                       tile_step=plan.tile_step, n_tiles=plan.n_tiles,
-                       compact=world > 1, stream=stream)
-    torch.cuda.synchronize()
-    fetch_sum, n_miss, n_unk, n_hit = (int(v) for v in out.stats.cpu())
-    n_local = n_miss + n_unk + n_hit
-    alg_bytes = 4 * fetch_sum + 12 * n_hit + 16 * n_local
-
+    stream = wl.stream
     ev = [(torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -343,21 +524,9 @@ def main():
         for k in range(args.steps):
             flush.fill_(float(k))            # L2 flush, outside the events
             ev[k][0].record(stream)
-            if world == 1:
-                dev.render_cameras(dps, g, cams, W, H, out, stream=stream)
-                ev[k][1].record(stream)
-            else:
-                dev.render_cameras(dps, g, cams, W, H, out,
-                                   tile_begin=plan.tile_begin,
-                                   tile_step=plan.tile_step,
-                                   n_tiles=plan.n_tiles, compact=True,
-                                   stream=stream)
-                ev[k][1].record(stream)
-                gat = pdist.gather_shards(plan, out.status, out.rgb)
-                if gat is not None:
-                    dev.untile(len(cams), W, H, world, gat[0], gat[1],
-                               frame_st, frame_rgb,
-                               shard_stride=plan.max_tiles, stream=stream)
+            wl.trace()
+            ev[k][1].record(stream)
+            wl.gather()
             ev[k][2].record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -365,65 +534,44 @@ def main():
         torch.cuda.synchronize()
     step_ms = sum(e[0].elapsed_time(e[2]) for e in ev)
     kern_ms = sum(e[0].elapsed_time(e[1]) for e in ev)
-    t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dvc)
+    t = torch.tensor([step_ms, kern_ms], dtype=torch.float64)
     if world > 1:
+        if args.dist_backend == "nccl":
+            t = t.to(dvc)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     step_ms, kern_ms_max = (float(v) for v in t.cpu())
 
-    rays_total = len(cams) * W * H * args.steps
-    value = rays_total / (step_ms * 1e-3) / 1e6
-    frames_per_s = len(cams) * args.steps / (step_ms * 1e-3)
+    value = wl.rays_per_step * args.steps / (step_ms * 1e-3) / 1e6
     kern_avg_ms = kern_ms / args.steps
     hbm, peak_kind = peaks()
     achieved = alg_bytes / (kern_avg_ms * 1e-3) / 1e9
 
-    # e2e: the public API with host buffers, per rank one view per call
-    e2e = None
-    if not args.no_e2e:
-        cam = cams[rank % len(cams)]
-        for _ in range(2):
-            render_frame(cfg.grid, cam, device=local)
-        n_e2e = max(3, min(args.steps, 20))
-        if world > 1:
-            tdist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            fr = render_frame(cfg.grid, cam, device=local)
-        e2e_s = time.perf_counter() - t0
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=dvc)
-        if world > 1:
-            tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
-        e2e_s = float(te.item())
-        n_px = W * H
-        e2e = {"value": world * n_e2e * n_px / e2e_s / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": 104,
-               "d2h_bytes_per_step": n_px * 12 + n_px + 32,
-               "api": "render_frame(ProbeGrid, Camera) -> Frame (host arrays)",
-               "frame_ms": e2e_s / n_e2e * 1e3}
-        del fr
-
+    e2e = None if args.no_e2e else e2e_measure(wl, args.steps, world, rank,
+                                               local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        stride = {"c1": 1, "c2": 1, "c3": 16}[args.config]
-        cpu = cpu_baseline(cfg, args.cpu_budget, stride)
+        cpu = cpu_baseline(wl.cfg, args.config, args.cpu_budget)
 
     if rank == 0:
+        kernel = ("trace_rays_kernel (binned)" if args.config == "c5"
+                  else "render_cameras_kernel")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if args.config in ("c1", "c2") else "strong",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded analytic room, ray-cast probe bake, "
-                    "seeded cameras)",
-            "config": config_record(cfg, args.config, world, views),
-            "frames_per_s": frames_per_s,
-            "kernel_mrays_s": len(cams) * W * H / world / (kern_avg_ms * 1e-3)
-                              / 1e6,
+                    "seeded cameras / rays)",
+            "config": config_record(wl.cfg, args.config, world,
+                                    wl.frames_per_step),
+            "frames_per_s": (wl.frames_per_step * args.steps / (step_ms * 1e-3)
+                             if wl.frames_per_step else None),
+            "kernel_mrays_s_per_gpu": n_local / (kern_avg_ms * 1e-3) / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "render_cameras_kernel",
+                         "kernel": kernel,
                          "alg_bytes_per_launch": alg_bytes,
                          "rays_per_launch": n_local,
                          "fetch_per_ray": fetch_sum / max(n_local, 1),
@@ -431,12 +579,14 @@ def main():
                          "avg_launch_ms": kern_avg_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": wl.launches_per_step() * args.steps,
+            "clocks": clocks.summary(),
             "trace_mode": args.mode,
             "lib": os.path.basename(os.environ.get("LFP_LIB_PATH", "")) or
                    "liblfprobe_b200.so",
-            "clocks": clocks.summary(),
         }
+        if args.dist_backend != "nccl":
+            line["dist_backend"] = args.dist_backend
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()

@@ -179,6 +179,22 @@ int lfp_trace_rays(const lfp_probeset* ps, const lfp_grid_params* grid,
                    const void* ray_origins, const void* ray_dirs, int32_t f32,
                    int64_t n, const lfp_outputs* out, void* stream);
 
+/* Ray binning for incoherent batches (config 5): keys[i] = 8 * (lattice
+ * cube where ray i enters the grid) + direction octant, 0xffffffff for rays
+ * missing the lattice. Sorting rays by key (any stable or unstable device
+ * sort) and tracing them in that order with lfp_trace_rays_ordered lets a
+ * warp march coherent cubes/segments; results do not depend on the order. */
+int lfp_bin_rays(const lfp_grid_params* grid, const void* ray_origins,
+                 const void* ray_dirs, int32_t f32, int64_t n, uint32_t* keys,
+                 void* stream);
+
+/* lfp_trace_rays where slot s traces ray order[s] (a permutation of
+ * 0..n-1, device int32); outputs are written at the ray's input index. */
+int lfp_trace_rays_ordered(const lfp_probeset* ps, const lfp_grid_params* grid,
+                           const void* ray_origins, const void* ray_dirs,
+                           int32_t f32, int64_t n, const int32_t* order,
+                           const lfp_outputs* out, void* stream);
+
 /* Scatter compact-tile outputs of `n_ranks` shards back into frame order.
  * Shard k traced tiles k, k + n_ranks, ...; its j-th tile sits at tile slot
  * k * shard_stride + j of the input (shard_stride = 0: shards packed

@@ -9,7 +9,8 @@ status codes and `TraceConfig`. Tracing runs in the CUDA library
 
 from .grid import MapChain, ProbeData, ProbeGrid, ProbeSet
 from .octmap import EMPTY_DISTANCE, oct_decode, oct_encode
-from .render import Camera, Frame, bench_views, psnr, render_frame, write_image
+from .render import (Camera, Frame, bench_views, psnr, render_frame,
+                     trace_rays, write_image)
 from .trace import HIT, MISS, UNKNOWN, TraceConfig
 
 __all__ = [
@@ -17,6 +18,7 @@ __all__ = [
     "HIT", "MISS", "UNKNOWN", "TraceConfig",
     "EMPTY_DISTANCE", "oct_encode", "oct_decode",
     "Camera", "Frame", "render_frame", "psnr", "bench_views", "write_image",
+    "trace_rays",
 ]
 
 __version__ = "0.1.0"

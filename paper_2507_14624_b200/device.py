@@ -210,6 +210,34 @@ def trace_rays(dps, gparams, origins, dirs, out, rgb_mode=1, stream=None):
         ctypes.c_void_p(st.cuda_stream)))
 
 
+def bin_rays(gparams, origins, dirs, stream=None):
+    """lfp_bin_rays -> uint32 keys as an int64 tensor-compatible int32 view."""
+    n = dirs.shape[0]
+    keys = torch.empty(n, dtype=torch.int32, device=dirs.device)
+    st = stream if stream is not None else torch.cuda.current_stream(dirs.device)
+    native.check(native.lib().lfp_bin_rays(
+        ctypes.byref(gparams), _ptr(origins), _ptr(dirs),
+        int(dirs.dtype == torch.float32), n, _ptr(keys),
+        ctypes.c_void_p(st.cuda_stream)))
+    return keys
+
+
+def ray_order(keys):
+    """Permutation sorting rays by bin key (unsigned order)."""
+    k = keys.to(torch.int64) & 0xFFFFFFFF
+    return torch.argsort(k).to(torch.int32)
+
+
+def trace_rays_ordered(dps, gparams, origins, dirs, order, out, rgb_mode=1,
+                       stream=None):
+    st = stream if stream is not None else torch.cuda.current_stream(dps.device)
+    o = out.struct(rgb_mode)
+    native.check(native.lib().lfp_trace_rays_ordered(
+        dps.handle, ctypes.byref(gparams), _ptr(origins), _ptr(dirs),
+        int(dirs.dtype == torch.float32), dirs.shape[0], _ptr(order),
+        ctypes.byref(o), ctypes.c_void_p(st.cuda_stream)))
+
+
 def render_grid_dirs(dps, gparams, eye, dirs, out, rgb_mode=1, stream=None):
     """lfp_render_grid: shared eye, device dirs (N, 3) f64/f32."""
     dirs = dirs.contiguous()

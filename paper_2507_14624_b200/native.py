@@ -104,11 +104,17 @@ def lib():
         L.lfp_trace_rays.argtypes = [
             vp, ctypes.POINTER(GridParams), vp, vp, i32, i64,
             ctypes.POINTER(Outputs), vp]
+        L.lfp_bin_rays.argtypes = [ctypes.POINTER(GridParams), vp, vp, i32,
+                                    i64, vp, vp]
+        L.lfp_trace_rays_ordered.argtypes = [
+            vp, ctypes.POINTER(GridParams), vp, vp, i32, i64, vp,
+            ctypes.POINTER(Outputs), vp]
         L.lfp_untile.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
         L.lfp_bake_probes.argtypes = [
             ctypes.c_int, ctypes.POINTER(PrimC), i32, ctypes.POINTER(LightC),
             vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-        for name in ("lfp_bake_probes", "lfp_render_probes",
+        for name in ("lfp_bin_rays", "lfp_trace_rays_ordered",
+                     "lfp_bake_probes", "lfp_render_probes",
                      "lfp_probeset_create", "lfp_probeset_destroy",
                      "lfp_probeset_info", "lfp_render_cameras",
                      "lfp_render_grid", "lfp_trace_rays", "lfp_untile"):
@@ -128,4 +134,5 @@ def exported_symbols():
     return ["lfp_version", "lfp_last_error", "lfp_probeset_create",
             "lfp_probeset_destroy", "lfp_probeset_info", "lfp_render_cameras",
             "lfp_num_tiles", "lfp_render_grid", "lfp_trace_rays",
-            "lfp_untile", "lfp_bake_probes", "lfp_render_probes"]
+            "lfp_untile", "lfp_bake_probes", "lfp_render_probes",
+            "lfp_bin_rays", "lfp_trace_rays_ordered"]
