@@ -120,6 +120,25 @@ int lfp_probeset_create(int device, const float* dist_hi, const float* dir_hi,
                         int32_t r, uint32_t flags, void* stream,
                         lfp_probeset** out);
 
+/* Same, straight from the .lfp payload sections (bake.py:228-341): per
+ * probe (concatenated over P probes, host memory) irradiance RGB565
+ * u16[R][R], distance f16[R][R], direction 2 x u8 sub-texel offsets
+ * [R][R][2], low-res distance f16[r][r]; origins f64[P][3] may be host or
+ * device (`origins` of lfp_probeset_create also accepts either). Uploads 6 B
+ * per texel instead of 28 and decodes on the device exactly as load_probe
+ * does (f32 RGB565 division, fp64 sub-texel oct_decode, EMPTY texels
+ * zeroed). The decoded reference-layout arrays are also written to the
+ * optional host buffers (for the Python ProbeSet mirror). Replaces
+ * load_probe / load_grid's host decode (bake.py:301-341, grid.py:268-274). */
+int lfp_probeset_create_packed(int device, const uint16_t* irr565,
+                               const uint16_t* dist_f16, const uint8_t* dir_q8,
+                               const uint16_t* dist_lo_f16,
+                               const double* origins, int64_t P, int32_t R,
+                               int32_t r, uint32_t flags, float* host_dist_hi,
+                               float* host_dir_hi, float* host_irr_hi,
+                               float* host_dist_lo, void* stream,
+                               lfp_probeset** out);
+
 int lfp_probeset_destroy(lfp_probeset* ps);
 
 /* Device bytes held by the probe set, and which payload formats it chose. */

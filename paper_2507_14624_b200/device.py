@@ -61,6 +61,17 @@ class DeviceProbeSet:
                                      handle)
 
     @classmethod
+    def from_handle(cls, handle, device, P, R, r):
+        """Wrap a handle created elsewhere (e.g. lfp_probeset_create_packed)."""
+        self = cls.__new__(cls)
+        self.device = device
+        self.handle = handle
+        self.P, self.R, self.r = P, R, r
+        self._fin = weakref.finalize(self, native.lib().lfp_probeset_destroy,
+                                     handle)
+        return self
+
+    @classmethod
     def from_probe_set(cls, ps, device=0, half="auto"):
         return cls(ps.dist_hi, ps.dir_hi, ps.irr_hi, ps.dist_lo, ps.origins,
                    device=device, half=half)
@@ -272,16 +283,22 @@ def cached_probe_set(dist_hi, dir_hi, irr_hi, dist_lo, origins, device=0):
     return cached_for(arrs, lambda: arrs, device)
 
 
-def cached_for(key_objs, arrays_fn, device=0):
+def register(dps, key_objs, device=0):
+    """Make `dps` the cached device copy for `key_objs` (weakly held)."""
+    return cached_for(key_objs, None, device, dps=dps)
+
+
+def cached_for(key_objs, arrays_fn, device=0, dps=None):
     """Device probe set cached on the identity of `key_objs` (weakly held);
     `arrays_fn()` yields the five host arrays on a miss."""
     key = tuple(id(a) for a in key_objs) + (int(device),)
-    hit = _CACHE.get(key)
+    hit = _CACHE.get(key) if dps is None else None
     if hit is not None:
-        refs, dps = hit
+        refs, cached = hit
         if all(r() is a for r, a in zip(refs, key_objs)):
-            return dps
-    dps = DeviceProbeSet(*arrays_fn(), device=device)
+            return cached
+    if dps is None:
+        dps = DeviceProbeSet(*arrays_fn(), device=device)
     try:
         refs = tuple(weakref.ref(a) for a in key_objs)
     except TypeError:

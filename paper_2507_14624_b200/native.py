@@ -85,6 +85,9 @@ def lib():
         L.lfp_probeset_create.argtypes = [
             ctypes.c_int, vp, vp, vp, vp, vp, i64, i32, i32, u32, vp,
             ctypes.POINTER(vp)]
+        L.lfp_probeset_create_packed.argtypes = [
+            ctypes.c_int, vp, vp, vp, vp, vp, i64, i32, i32, u32, vp, vp, vp,
+            vp, vp, ctypes.POINTER(vp)]
         L.lfp_probeset_destroy.argtypes = [vp]
         L.lfp_probeset_info.argtypes = [vp, ctypes.POINTER(i64),
                                         ctypes.POINTER(i32),
@@ -113,7 +116,7 @@ def lib():
         L.lfp_bake_probes.argtypes = [
             ctypes.c_int, ctypes.POINTER(PrimC), i32, ctypes.POINTER(LightC),
             vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-        for name in ("lfp_bin_rays", "lfp_trace_rays_ordered",
+        for name in ("lfp_probeset_create_packed", "lfp_bin_rays", "lfp_trace_rays_ordered",
                      "lfp_bake_probes", "lfp_render_probes",
                      "lfp_probeset_create", "lfp_probeset_destroy",
                      "lfp_probeset_info", "lfp_render_cameras",
@@ -135,4 +138,5 @@ def exported_symbols():
             "lfp_probeset_destroy", "lfp_probeset_info", "lfp_render_cameras",
             "lfp_num_tiles", "lfp_render_grid", "lfp_trace_rays",
             "lfp_untile", "lfp_bake_probes", "lfp_render_probes",
-            "lfp_bin_rays", "lfp_trace_rays_ordered"]
+            "lfp_bin_rays", "lfp_trace_rays_ordered",
+            "lfp_probeset_create_packed"]

@@ -453,3 +453,43 @@ class TestNonGridSources:
             assert fr.stats["perPixelTexelFetches"] == 1.0
         else:
             assert fr.stats["unknownFraction"] > 0.1   # UNKNOWN -> magenta
+
+
+class TestLfpLoad:
+    """.lfp files written by the reference, decoded on the GPU
+    (lfp_probeset_create_packed) == the reference loader's arrays; the
+    loaded grid renders the reference frame."""
+
+    def test_load_grid_matches_reference_loader(self, golden):
+        import os
+        from conftest import GOLDEN
+        from paper_2507_14624_b200 import lfpio, render_frame
+        z = golden("lfp")
+        grid = lfpio.load_grid(os.path.join(GOLDEN, "lfp_grid", "grid.json"))
+        ps = grid.probe_set
+        for k in ("dist_hi", "dir_hi", "irr_hi", "dist_lo", "origins"):
+            np.testing.assert_array_equal(getattr(ps, k), z[k], err_msg=k)
+        assert grid.dims == tuple(int(v) for v in z["dims"])
+        fr = render_frame(grid, golden_camera(z))
+        np.testing.assert_array_equal(fr.status, z["cam_frame_status"])
+        np.testing.assert_array_equal(fr.pixels, z["cam_frame_pixels"])
+
+    def test_load_probe_and_format_errors(self, golden, tmp_path):
+        import os
+        from conftest import GOLDEN
+        from paper_2507_14624_b200 import lfpio
+        z = golden("lfp")
+        src = os.path.join(GOLDEN, "lfp_grid", "probe_1_0_1.lfp")
+        p = lfpio.load_probe(src)
+        idx = (1 * 2 + 0) * 2 + 1
+        np.testing.assert_array_equal(p.chain.distance_hi, z["dist_hi"][idx])
+        np.testing.assert_array_equal(p.chain.direction_hi, z["dir_hi"][idx])
+        np.testing.assert_array_equal(p.chain.irradiance_hi, z["irr_hi"][idx])
+        data = open(src, "rb").read()
+        bad = tmp_path / "bad.lfp"
+        bad.write_bytes(b"NOTPROBE" + data[8:])
+        with pytest.raises(lfpio.ProbeFormatError, match="bad magic"):
+            lfpio.load_probe(str(bad))
+        bad.write_bytes(data[:-3])
+        with pytest.raises(lfpio.ProbeFormatError, match="expected"):
+            lfpio.load_probe(str(bad))
