@@ -198,9 +198,10 @@ int lfp_trace_rays(const lfp_probeset* ps, const lfp_grid_params* grid,
                    const void* ray_origins, const void* ray_dirs, int32_t f32,
                    int64_t n, const lfp_outputs* out, void* stream);
 
-/* Ray binning for incoherent batches (config 5): keys[i] = 8 * (lattice
- * cube where ray i enters the grid) + direction octant, 0xffffffff for rays
- * missing the lattice. Sorting rays by key (any stable or unstable device
+/* Ray binning for incoherent batches (config 5): keys[i] = (lattice cube
+ * where ray i enters the grid, 4x4x4 sub-cell of the entry point, 8x8
+ * octahedral cell of the direction), 0xffffffff for rays missing the
+ * lattice (cubes < 2^20). Sorting rays by key (any stable or unstable device
  * sort) and tracing them in that order with lfp_trace_rays_ordered lets a
  * warp march coherent cubes/segments; results do not depend on the order. */
 int lfp_bin_rays(const lfp_grid_params* grid, const void* ray_origins,
