@@ -48,6 +48,16 @@ _REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting",
             0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
+def ncu_traffic(config):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)[config]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
@@ -138,6 +148,8 @@ def build_config(name, views):
         return configs.c2(n_views=views)
     if name in ("c3", "c5"):
         return configs.c3(n_views=views)
+    if name == "c4":
+        return configs.c4(n_views=views)
     raise SystemExit(f"unknown config {name}")
 
 
@@ -150,6 +162,10 @@ def config_record(cfg, name, world, views):
         "l2": "flushed between steps (512 MiB write, outside timed events)",
         "seeds": "configs.py (scene/bake/camera/ray seeds fixed)",
     }
+    if getattr(cfg, "levels", None):
+        rec["levels"] = [{"dims": list(g.dims), "cell": g.cell_size,
+                          "probes": int(g.probe_set.n_probes)} for g in cfg.levels]
+        rec["probes"] = sum(l["probes"] for l in rec["levels"])
     if name == "c5":
         rec.update({"workload": "C5: incoherent-ray stress, 2^26 f32 rays "
                                 "(origins U(room), directions normalised "
@@ -191,15 +207,18 @@ def cpu_sample(cfg, name, stride):
 
 def run_cpu(cfg, eye, dirs):
     from oracle import oracle
-    g = cfg.grid
     t0 = time.perf_counter()
-    res = oracle.trace_rays(g.probe_set, g.grid_origin, g.cell_size, g.dims,
-                            eye, dirs)
+    if getattr(cfg, "levels", None):
+        res = oracle.trace_hierarchy(cfg.levels, eye, dirs)
+    else:
+        g = cfg.grid
+        res = oracle.trace_rays(g.probe_set, g.grid_origin, g.cell_size,
+                                g.dims, eye, dirs)
     return time.perf_counter() - t0, res
 
 
-CPU_STRIDE = {"c1": 1, "c2": 1, "c3": 16, "c5": 256}
-REF_STRIDE = {"c1": 1, "c2": 4, "c3": 64, "c5": 512}
+CPU_STRIDE = {"c1": 1, "c2": 1, "c3": 16, "c4": 64, "c5": 256}
+REF_STRIDE = {"c1": 1, "c2": 4, "c3": 64, "c4": 256, "c5": 512}
 
 
 def cpu_baseline(cfg, name, budget_s=12.0):
@@ -287,7 +306,7 @@ class Workload:
         self.name, self.world, self.rank, self.dvc = args.config, world, rank, dvc
         self.gather_backend = args.dist_backend
         name = args.config
-        if name in ("c1", "c2"):
+        if name in ("c1", "c2", "c4"):
             self.views = args.views or 1
             views_total = self.views * world          # weak scaling
         elif name == "c3":
@@ -296,6 +315,13 @@ class Workload:
             self.views = views_total = 1
         self.cfg = build_config(name, views_total)
         self.dps = device_probe_set(self.cfg.grid, dvc.index)
+        self.levels = None
+        if name == "c4":
+            self.levels = [(device_probe_set(gr, dvc.index),
+                            dev.grid_params(gr.grid_origin, gr.cell_size,
+                                            gr.dims, DEFAULT_CONFIG,
+                                            mode=args.mode))
+                           for gr in self.cfg.levels]
         self.g = dev.grid_params(self.cfg.grid.grid_origin,
                                  self.cfg.grid.cell_size, self.cfg.grid.dims,
                                  DEFAULT_CONFIG, mode=args.mode)
@@ -351,7 +377,17 @@ class Workload:
                 dev.trace_rays(self.dps, self.g, self.o, self.d, self.out,
                                stream=self.stream)
             return
-        if self.world == 1:
+        if self.levels is not None:
+            if self.world == 1:
+                dev.render_hierarchy(self.levels, self.cams, self.W, self.H,
+                                     self.out, stream=self.stream)
+            else:
+                dev.render_hierarchy(self.levels, self.cams, self.W, self.H,
+                                     self.out, tile_begin=self.plan.tile_begin,
+                                     tile_step=self.plan.tile_step,
+                                     n_tiles=self.plan.n_tiles, compact=True,
+                                     stream=self.stream)
+        elif self.world == 1:
             dev.render_cameras(self.dps, self.g, self.cams, self.W, self.H,
                                self.out, stream=self.stream)
         else:
@@ -464,7 +500,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--config", default="c2",
+                    choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--views", type=int, default=0,
                     help="views per step (per GPU for c1/c2, total for c3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -553,15 +590,16 @@ def main():
         cpu = cpu_baseline(wl.cfg, args.config, args.cpu_budget)
 
     if rank == 0:
-        kernel = ("trace_rays_kernel (binned)" if args.config == "c5"
-                  else "render_cameras_kernel")
+        kernel = {"c5": "trace_rays_kernel (binned)",
+                  "c4": "render_hierarchy_kernel"}.get(args.config,
+                                                       "render_cameras_kernel")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak" if args.config in ("c1", "c2") else "strong",
+            "scaling": "weak" if args.config in ("c1", "c2", "c4") else "strong",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded analytic room, ray-cast probe bake, "
+            "data": "synthetic (seeded analytic scene, ray-cast probe bake, "
                     "seeded cameras / rays)",
             "config": config_record(wl.cfg, args.config, world,
                                     wl.frames_per_step),
@@ -570,7 +608,9 @@ def main():
             "kernel_mrays_s_per_gpu": n_local / (kern_avg_ms * 1e-3) / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "peak_kind": peak_kind,
+                         "traffic": ncu_traffic(args.config),
+                         "traffic_unit": "bytes per launch (ncu, cold cache)",
+                         "peak_kind": peak_kind,
                          "kernel": kernel,
                          "alg_bytes_per_launch": alg_bytes,
                          "rays_per_launch": n_local,

@@ -182,6 +182,20 @@ int lfp_render_probes(const lfp_probeset* ps, int32_t source_kind,
                       int32_t n_cams, int32_t width, int32_t height,
                       const lfp_outputs* out, void* stream);
 
+/* Coarse-to-fine probe hierarchy (config 4): up to 4 probe-grid levels on
+ * one device, each with its own lattice (grids[l]); every pixel ray is traced
+ * through level 0 (kernels.py:653-822), a MISS falls through to level 1, and
+ * so on; the first HIT wins. fetch = sum over the levels tried; the probe
+ * output is (level << 24) | probe (HIT, or the last MISS diagnostic); texel,
+ * rgb, hit_t refer to that level's probe. Same tiling / compact layout as
+ * lfp_render_cameras; all levels share grids[0].trace_mode. */
+int lfp_render_hierarchy(const lfp_probeset* const* levels,
+                         const lfp_grid_params* grids, int32_t n_levels,
+                         const lfp_camera* cams_host, int32_t n_cams,
+                         int32_t width, int32_t height, int64_t tile_begin,
+                         int64_t tile_step, int64_t n_tiles, int32_t compact,
+                         const lfp_outputs* out, void* stream);
+
 /* Number of 8x16 tiles of a batch of n_cams frames of width x height. */
 int64_t lfp_num_tiles(int32_t n_cams, int32_t width, int32_t height);
 

@@ -164,6 +164,37 @@ def frame_pixels(res, height, width, background=(0.0, 0.0, 0.0),
     return rgb.reshape(height, width, 3), res.status.reshape(height, width)
 
 
+def trace_hierarchy(levels, eye, dirs):
+    """Coarse-to-fine composition of per-level oracle traces (the reference
+    has no hierarchy): MISS rays re-trace on the next
+    level, fetches add up, first HIT wins."""
+    n = len(dirs)
+    out = Result(n)
+    out.probe[:] = -1
+    out.tx[:] = -1
+    out.ty[:] = -1
+    todo = np.arange(n)
+    for lvl, g in enumerate(levels):
+        if len(todo) == 0:
+            break
+        o = eye if np.ndim(eye) == 1 else eye[todo]
+        r = trace_rays(g.probe_set, g.grid_origin, g.cell_size, g.dims,
+                              o, dirs[todo])
+        out.fetch[todo] += r.fetch
+        hit = r.status == 1
+        diag = (~hit) & (r.probe >= 0)
+        for m in (hit, diag):
+            idx = todo[m]
+            out.probe[idx] = (lvl << 24) | r.probe[m]
+            out.tx[idx] = r.tx[m]
+            out.ty[idx] = r.ty[m]
+        out.status[todo[hit]] = 1
+        out.rgb[todo[hit]] = r.rgb[hit]
+        todo = todo[~hit]
+    return out
+
+
+
 def oct_encode(d):
     out = np.empty(2)
     lib().lfpo_oct_encode(float(d[0]), float(d[1]), float(d[2]), out)

@@ -23,7 +23,7 @@ import numpy as np
 from .bake import bake_grid, bake_grid_gpu
 from .grid import ProbeGrid
 from .render import Camera
-from .scenes import free_point, room_scene
+from .scenes import city_scene, free_point, room_scene
 
 
 @dataclass
@@ -99,6 +99,64 @@ def c3(seed=303, cam_seed=3303, n_views=64, width=1920, height=1080,
                   f"{n_views} poses at {width}x{height}")
 
 
+C4_LEVELS = (((8, 2, 8), 64.0 / 7.0), ((16, 4, 16), 64.0 / 15.0),
+             ((32, 8, 32), 64.0 / 31.0))
+
+
+def c4_levels(seed=404, device=0, levels=C4_LEVELS, r_hi=128, r_lo=32):
+    """C4 probe hierarchy: three lattices over the 64 x 64 m block (8x2x8,
+    16x4x16, 32x8x32 probes, cubic cells 64/7, 64/15, 64/31 m; y spans 9.1 /
+    12.8 / 14.5 m), 128^2 / 32^2 maps, f16 radiance / direction, all baked
+    on the GPU against the 2001 primitives. Returns (scene, [ProbeGrid])."""
+    scene = city_scene(seed)
+    grids = [bake_grid_gpu(scene, (0.0, 0.0, 0.0), cell, dims, r_hi, r_lo,
+                           quant="f16", device=device)
+             for dims, cell in levels]
+    return scene, grids
+
+
+def street_cameras(scene, n, width, height, seed, vfov=60.0):
+    """Eyes 1.5-12 m above the ground at free points of the block, looking
+    across it with a slight downward pitch."""
+    rng = np.random.default_rng(seed)
+    cams = []
+    for _ in range(n):
+        for _ in range(1000):
+            eye = free_point(scene, rng, margin=4.0)
+            eye[1] = rng.uniform(1.5, 12.0)
+            if free_point_ok(scene, eye):
+                break
+        yaw = rng.uniform(0.0, 2.0 * np.pi)
+        pitch = np.radians(rng.uniform(-25.0, 0.0))
+        fwd = (np.cos(pitch) * np.cos(yaw), np.sin(pitch),
+               np.cos(pitch) * np.sin(yaw))
+        cams.append(Camera(eye=tuple(float(v) for v in eye),
+                           forward=tuple(float(v) for v in fwd),
+                           vfov_deg=vfov, width=width, height=height))
+    return cams
+
+
+def free_point_ok(scene, p):
+    from .scenes import Box, scene_skip
+    for prim in scene.primitives[scene_skip(scene):]:
+        if isinstance(prim, Box) and np.all(p > np.asarray(prim.lo) - 0.05) \
+                and np.all(p < np.asarray(prim.hi) + 0.05):
+            return False
+    return True
+
+
+def c4(seed=404, cam_seed=4404, n_views=1, width=3840, height=2160, device=0):
+    scene, grids = c4_levels(seed, device)
+    cams = street_cameras(scene, n_views, width, height, cam_seed)
+    cfg = Config("c4", scene, grids[-1], cams,
+                 "block 64x64x16 m, ground + 2000 boxes (lognormal heights); "
+                 "3-level probe hierarchy 8x2x8 / 16x4x16 / 32x8x32 at "
+                 f"128^2/32^2 (f16 payloads), coarse-to-fine; {n_views} view(s) "
+                 f"at {width}x{height}")
+    cfg.levels = grids
+    return cfg
+
+
 def c5_rays(scene, n, seed=505):
     """Incoherent rays: origins U(interior), directions normalised Gaussian
     (`pkg/tests/conftest.py:29-31`), both stored as float32."""
@@ -118,4 +176,4 @@ def probe_set_digest(ps):
     return h.hexdigest()
 
 
-BUILDERS = {"c1": c1, "c2": c2, "c3": c3}
+BUILDERS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4}

@@ -205,6 +205,29 @@ def render_probes(dps, kind, cams, width, height, out, gparams, order=None,
         ctypes.c_void_p(st.cuda_stream)))
 
 
+def render_hierarchy(levels, cams, width, height, out, tile_begin=0,
+                     tile_step=1, n_tiles=None, compact=False,
+                     background=(0.0, 0.0, 0.0), unknown_color=(1.0, 0.0, 1.0),
+                     stream=None):
+    """lfp_render_hierarchy: `levels` is a list of (DeviceProbeSet,
+    GridParams), coarse first."""
+    n = len(levels)
+    handles = (ctypes.c_void_p * n)(*[l[0].handle.value for l in levels])
+    grids = (native.GridParams * n)(*[l[1] for l in levels])
+    cams_c = (native.CameraC * len(cams))(*[camera_struct(c) for c in cams])
+    total = num_tiles(len(cams), width, height)
+    if n_tiles is None:
+        n_tiles = (total - tile_begin + tile_step - 1) // tile_step
+    st = stream if stream is not None else torch.cuda.current_stream(
+        levels[0][0].device)
+    o = out.struct(0, background, unknown_color)
+    native.check(native.lib().lfp_render_hierarchy(
+        handles, grids, n, cams_c, len(cams), width, height, tile_begin,
+        tile_step, n_tiles, int(compact), ctypes.byref(o),
+        ctypes.c_void_p(st.cuda_stream)))
+    return n_tiles
+
+
 def trace_rays(dps, gparams, origins, dirs, out, rgb_mode=1, stream=None):
     """lfp_trace_rays: origins/dirs are device tensors (N, 3), both f64 or
     both f32."""

@@ -99,6 +99,10 @@ def lib():
             vp, i32, ctypes.POINTER(i32), i32, ctypes.POINTER(ctypes.c_double),
             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(GridParams),
             ctypes.POINTER(CameraC), i32, i32, i32, ctypes.POINTER(Outputs), vp]
+        L.lfp_render_hierarchy.argtypes = [
+            ctypes.POINTER(vp), ctypes.POINTER(GridParams), i32,
+            ctypes.POINTER(CameraC), i32, i32, i32, i64, i64, i64, i32,
+            ctypes.POINTER(Outputs), vp]
         L.lfp_num_tiles.argtypes = [i32, i32, i32]
         L.lfp_num_tiles.restype = i64
         L.lfp_render_grid.argtypes = [
@@ -116,7 +120,8 @@ def lib():
         L.lfp_bake_probes.argtypes = [
             ctypes.c_int, ctypes.POINTER(PrimC), i32, ctypes.POINTER(LightC),
             vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-        for name in ("lfp_probeset_create_packed", "lfp_bin_rays", "lfp_trace_rays_ordered",
+        for name in ("lfp_render_hierarchy", "lfp_probeset_create_packed",
+                     "lfp_bin_rays", "lfp_trace_rays_ordered",
                      "lfp_bake_probes", "lfp_render_probes",
                      "lfp_probeset_create", "lfp_probeset_destroy",
                      "lfp_probeset_info", "lfp_render_cameras",
@@ -139,4 +144,4 @@ def exported_symbols():
             "lfp_num_tiles", "lfp_render_grid", "lfp_trace_rays",
             "lfp_untile", "lfp_bake_probes", "lfp_render_probes",
             "lfp_bin_rays", "lfp_trace_rays_ordered",
-            "lfp_probeset_create_packed"]
+            "lfp_probeset_create_packed", "lfp_render_hierarchy"]

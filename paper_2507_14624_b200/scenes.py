@@ -217,6 +217,39 @@ def room_scene(seed, size=(4.0, 3.0, 4.0), n_boxes=8, n_spheres=4,
     return Scene(tuple(prims), light, (0.0, 0.0, 0.0), (w, h, l))
 
 
+def city_scene(seed, size=64.0, height=16.0, n_boxes=2000,
+               footprint=(1.0, 4.0), height_mu=1.0, height_sigma=0.5):
+    """Seeded block-scale scene (BASELINE config 4): a 64 x 64 m ground slab
+    and `n_boxes` axis-aligned buildings with footprint sides U[1, 4] m
+    (the footprint distribution is this builder's choice) and heights
+    exp(N(mu = 1, sigma = 0.5)) m clipped to the 16 m scene height, placed
+    uniformly (overlaps allowed), albedo U[0.2, 0.9]^3, one high point
+    light. Open sky: rays that leave the scene hit nothing (EMPTY texels)."""
+    rng = np.random.default_rng(seed)
+    prims = [Box((0.0, -1.0, 0.0), (size, 0.0, size),
+                 tuple(rng.uniform(0.2, 0.9, 3)))]
+    for _ in range(n_boxes):
+        sx, sz = rng.uniform(*footprint, 2)
+        h = float(np.clip(np.exp(rng.normal(height_mu, height_sigma)), 0.2,
+                          height - 0.5))
+        x = rng.uniform(0.0, size - sx)
+        z = rng.uniform(0.0, size - sz)
+        prims.append(Box((x, 0.0, z), (x + sx, h, z + sz),
+                         tuple(rng.uniform(0.2, 0.9, 3))))
+    light = PointLight((0.45 * size, 3.0 * height, 0.35 * size),
+                       power=4.0 * size * size, ambient=0.15)
+    return Scene(tuple(prims), light, (0.0, 0.0, 0.0), (size, height, size))
+
+
+def scene_skip(scene):
+    """Leading primitives that bound the scene (room walls / ground slab)
+    and may contain camera positions."""
+    p0 = scene.primitives[0] if scene.primitives else None
+    if isinstance(p0, Box) and p0.hi[1] <= 0.0:     # ground slab (city)
+        return 1
+    return 6                                          # six room walls
+
+
 def free_point(scene, rng, margin=0.3, tries=1000):
     """A point in the interior at least `margin` from the walls and outside
     every box/sphere (camera placement)."""
@@ -225,7 +258,7 @@ def free_point(scene, rng, margin=0.3, tries=1000):
     for _ in range(tries):
         p = rng.uniform(lo, hi)
         ok = True
-        for prim in scene.primitives[6:]:
+        for prim in scene.primitives[scene_skip(scene):]:
             if isinstance(prim, Box):
                 if np.all(p > np.asarray(prim.lo) - 0.05) and np.all(
                         p < np.asarray(prim.hi) + 0.05):

@@ -493,3 +493,40 @@ class TestLfpLoad:
         bad.write_bytes(data[:-3])
         with pytest.raises(lfpio.ProbeFormatError, match="expected"):
             lfpio.load_probe(str(bad))
+
+
+class TestHierarchy:
+    """Config-4 coarse-to-fine hierarchy (lfp_render_hierarchy) vs the
+    oracle's per-level composition, on the C4 block scene with the three
+    C4 lattices at reduced map resolution (32^2 / 8^2)."""
+
+    def test_hierarchy_vs_oracle(self):
+        from oracle import oracle
+        from paper_2507_14624_b200 import configs
+        from paper_2507_14624_b200 import device as dev
+        from paper_2507_14624_b200.render import device_probe_set
+        from paper_2507_14624_b200.trace import DEFAULT_CONFIG
+        scene, grids = configs.c4_levels(r_hi=32, r_lo=8)
+        cam = configs.street_cameras(scene, 1, 240, 136, 4404)[0]
+        levels = [(device_probe_set(g), dev.grid_params(
+            g.grid_origin, g.cell_size, g.dims, DEFAULT_CONFIG)) for g in grids]
+        n = cam.width * cam.height
+        out = dev.RayOutputs(n, levels[0][0].device, probe=True, texel=True,
+                             fetch=True)
+        dev.render_hierarchy(levels, [cam], cam.width, cam.height, out)
+        torch.cuda.synchronize()
+        basis, tv, th = oracle.camera_params(cam)
+        dirs = oracle.camera_dirs(basis, tv, th, cam.width, cam.height)
+        exp = oracle.trace_hierarchy(grids, np.asarray(cam.eye, np.float64), dirs)
+        tex = out.texel.cpu().numpy()
+        got = dict(status=out.status.cpu().numpy(), probe=out.probe.cpu().numpy(),
+                   tx=np.where(tex < 0, -1, tex & 0xFFFF),
+                   ty=np.where(tex < 0, -1, tex >> 16),
+                   fetch=out.fetch.cpu().numpy())
+        for k in ("status", "probe", "tx", "ty", "fetch"):
+            np.testing.assert_array_equal(got[k], getattr(exp, k), err_msg=k)
+        hit = got["status"] == 1
+        np.testing.assert_array_equal(out.rgb.cpu().numpy()[hit],
+                                      exp.rgb[hit].astype(np.float32))
+        lv = got["probe"][hit] >> 24
+        assert hit.mean() > 0.3 and len(np.unique(lv)) >= 2   # >1 level used
