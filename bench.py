@@ -324,7 +324,9 @@ class Workload:
                            for gr in self.cfg.levels]
         self.g = dev.grid_params(self.cfg.grid.grid_origin,
                                  self.cfg.grid.cell_size, self.cfg.grid.dims,
-                                 DEFAULT_CONFIG, mode=args.mode)
+                                 DEFAULT_CONFIG, mode=args.mode,
+                                 schedule=args.schedule,
+                                 min_active=args.min_active)
         self.stream = torch.cuda.current_stream(dvc)
         self.extra_in_bytes = 0
         if name == "c5":
@@ -513,6 +515,12 @@ def main():
                     choices=["filtered", "exact", "check"],
                     help="trace_mode: fp32 decision filters + exact fallback "
                          "(default), exact fp64 only, or self-check")
+    ap.add_argument("--schedule", default="default",
+                    choices=["default", "nested", "persistent"],
+                    help="traversal schedule (default: nested for cameras, "
+                         "persistent for explicit rays)")
+    ap.add_argument("--min-active", type=int, default=0,
+                    help="persistent schedule stepping threshold (0 = 16)")
     ap.add_argument("--lib", default=None,
                     help="alternative liblfprobe_b200 build (LFP_LIB_PATH)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -622,6 +630,7 @@ def main():
             "gpu_launches": wl.launches_per_step() * args.steps,
             "clocks": clocks.summary(),
             "trace_mode": args.mode,
+            "schedule": args.schedule,
             "lib": os.path.basename(os.environ.get("LFP_LIB_PATH", "")) or
                    "liblfprobe_b200.so",
         }

@@ -60,6 +60,13 @@ typedef struct {
                                the reference; 1 = exact fp64 on every step;
                                2 = filtered + re-check of every filtered
                                decision (counts into lfp_outputs.diag)    */
+    int32_t schedule;       /* 0 = entry point default (cameras: nested,
+                               explicit rays: persistent); 1 = nested: one
+                               thread per ray; 2 = persistent: flattened
+                               per-lane state machine, lanes pull rays from
+                               a global counter                           */
+    int32_t min_active;     /* persistent: keep stepping while >= this many
+                               lanes of a warp step (1..32, 0 = 16)      */
 } lfp_grid_params;
 
 /* Pinhole camera (render.py:24-62). `basis` = (right, up, forward) exactly

@@ -91,10 +91,11 @@ class DeviceProbeSet:
 
 
 TRACE_MODES = {"filtered": 0, "exact": 1, "check": 2}
+SCHEDULES = {"default": 0, "nested": 1, "persistent": 2}
 
 
 def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG,
-                mode="filtered"):
+                mode="filtered", schedule="default", min_active=0):
     g = native.GridParams()
     for k in range(3):
         g.grid_origin[k] = float(grid_origin[k])
@@ -104,6 +105,8 @@ def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG,
     g.eps_align = float(config.eps_align)
     g.slack = float(config.slack)
     g.trace_mode = TRACE_MODES[mode]
+    g.schedule = SCHEDULES[schedule]
+    g.min_active = int(min_active)
     return g
 
 

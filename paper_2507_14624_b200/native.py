@@ -36,7 +36,9 @@ class GridParams(ctypes.Structure):
                 ("eps_start", ctypes.c_double),
                 ("eps_align", ctypes.c_double),
                 ("slack", ctypes.c_double),
-                ("trace_mode", ctypes.c_int32)]
+                ("trace_mode", ctypes.c_int32),
+                ("schedule", ctypes.c_int32),
+                ("min_active", ctypes.c_int32)]
 
 
 class CameraC(ctypes.Structure):

@@ -530,3 +530,93 @@ class TestHierarchy:
                                       exp.rgb[hit].astype(np.float32))
         lv = got["probe"][hit] >> 24
         assert hit.mean() > 0.3 and len(np.unique(lv)) >= 2   # >1 level used
+
+
+class TestPersistentSchedule:
+    """The persistent flattened traversal (schedule 'persistent') produces
+    exactly the nested traversal's outputs (and hence the reference's)."""
+
+    def _run(self, grid, o, d, schedule, mode="filtered", min_active=0,
+             ordered=False):
+        dev = _dev()
+        from paper_2507_14624_b200.render import device_probe_set
+        from paper_2507_14624_b200.trace import DEFAULT_CONFIG
+        dps = device_probe_set(grid)
+        g = dev.grid_params(grid.grid_origin, grid.cell_size, grid.dims,
+                            DEFAULT_CONFIG, mode=mode, schedule=schedule,
+                            min_active=min_active)
+        dt = torch.float32 if d.dtype == np.float32 else torch.float64
+        n = len(d)
+        o = np.broadcast_to(np.asarray(o), (n, 3))
+        to = torch.as_tensor(np.ascontiguousarray(o), dtype=dt).cuda()
+        td = torch.as_tensor(np.ascontiguousarray(d), dtype=dt).cuda()
+        out = dev.RayOutputs(n, dps.device, probe=True, texel=True, fetch=True,
+                             hit_t=True, diag=True)
+        out.rgb.zero_()
+        if ordered:
+            order = dev.ray_order(dev.bin_rays(g, to, td))
+            dev.trace_rays_ordered(dps, g, to, td, order, out)
+        else:
+            dev.trace_rays(dps, g, to, td, out)
+        torch.cuda.synchronize()
+        return {k: getattr(out, k).cpu().numpy() for k in
+                ("status", "probe", "texel", "fetch", "rgb", "hit_t", "stats",
+                 "diag")}
+
+    def _same(self, a, b):
+        for k in ("status", "probe", "texel", "fetch", "rgb", "hit_t", "stats"):
+            np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+    @pytest.mark.parametrize("min_active", [1, 16, 32])
+    def test_pcgrid_incoherent(self, golden, min_active):
+        z = golden("pcgrid")
+        grid = golden_grid(z)
+        a = self._run(grid, z["inc_origins"], z["inc_dirs"], "nested")
+        b = self._run(grid, z["inc_origins"], z["inc_dirs"], "persistent",
+                      min_active=min_active)
+        self._same(a, b)
+        np.testing.assert_array_equal(b["status"], z["inc_status"])
+        np.testing.assert_array_equal(b["fetch"], z["inc_fetch"])
+
+    def test_c5_binned_and_check(self):
+        from paper_2507_14624_b200 import configs
+        scene, grid = configs.c3_grid()
+        o32, d32 = configs.c5_rays(scene, 1 << 17, seed=525)
+        a = self._run(grid, o32, d32, "nested")
+        b = self._run(grid, o32, d32, "persistent", ordered=True)
+        c = self._run(grid, o32, d32, "persistent", mode="check")
+        self._same(a, b)
+        self._same(a, c)
+        assert int(c["diag"][4]) == 0
+
+    def test_camera_persistent(self):
+        from paper_2507_14624_b200 import configs
+        from paper_2507_14624_b200 import device as dev
+        from paper_2507_14624_b200.render import device_probe_set
+        from paper_2507_14624_b200.trace import DEFAULT_CONFIG
+        cfg = configs.c2()
+        cams = cfg.cameras + configs.random_cameras(cfg.scene, 1, 512, 512, 77)
+        W, H = 500, 333
+        cams = [type(c)(eye=c.eye, forward=c.forward, width=W, height=H)
+                for c in cams]
+        dps = device_probe_set(cfg.grid)
+        res = []
+        for sched in ("nested", "persistent"):
+            g = dev.grid_params(cfg.grid.grid_origin, cfg.grid.cell_size,
+                                cfg.grid.dims, DEFAULT_CONFIG, schedule=sched)
+            out = dev.RayOutputs(len(cams) * W * H, dps.device, probe=True,
+                                 texel=True, fetch=True)
+            dev.render_cameras(dps, g, cams, W, H, out)
+            torch.cuda.synchronize()
+            res.append({k: getattr(out, k).cpu().numpy() for k in
+                        ("status", "rgb", "probe", "texel", "fetch", "stats")})
+            # compact shards too
+            T = dev.num_tiles(len(cams), W, H)
+            o2 = dev.RayOutputs(((T + 2) // 3) * 128, dps.device, fetch=True)
+            o2.status.fill_(255)
+            dev.render_cameras(dps, g, cams, W, H, o2, tile_begin=1,
+                               tile_step=3, compact=True)
+            torch.cuda.synchronize()
+            res[-1]["compact"] = o2.status.cpu().numpy()
+        for k in res[0]:
+            np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)

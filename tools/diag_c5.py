@@ -20,10 +20,13 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
 scene, grid = configs.c3_grid()
 o, d = configs.c5_rays(scene, n, seed=505)
 dps = device_probe_set(grid)
-g = dev.grid_params(grid.grid_origin, grid.cell_size, grid.dims, DEFAULT_CONFIG)
 to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
 res = {"rays": n}
-for binned in (False, True):
+variants = [("nested", 0, False), ("nested", 0, True)] + [
+    ("persistent", ma, b) for ma in (8, 16, 24) for b in (False, True)]
+for sched, ma, binned in variants:
+    g = dev.grid_params(grid.grid_origin, grid.cell_size, grid.dims,
+                        DEFAULT_CONFIG, schedule=sched, min_active=ma)
     out = dev.RayOutputs(n, dps.device, fetch=True, diag=True)
     for it in range(2):
         out.diag.zero_()
@@ -42,7 +45,7 @@ for binned in (False, True):
         torch.cuda.synchronize()
     f = out.fetch.cpu().numpy()
     dg = [int(v) for v in out.diag.cpu()]
-    res["binned" if binned else "unbinned"] = {
+    res[f"{sched}_ma{ma}_{'binned' if binned else 'unbinned'}"] = {
         "sort_ms": e0.elapsed_time(e1), "trace_ms": e1.elapsed_time(e2),
         "lo": dg[0] + dg[1], "lo_rseg": dg[5], "hi": dg[2] + dg[3],
         "hi_sq": dg[6], "segs": dg[7], "lo_slow": dg[1], "hi_slow": dg[3],
