@@ -474,7 +474,8 @@ def e2e_measure(wl, steps, world, rank, local):
     else:
         cam = wl.cams[rank % len(wl.cams)]
         n = cam.width * cam.height
-        call = lambda: pkg.render_frame(wl.cfg.grid, cam, device=local)  # noqa: E731
+        src = getattr(wl.cfg, "hierarchy", None) or wl.cfg.grid
+        call = lambda: pkg.render_frame(src, cam, device=local)  # noqa: E731
         call()
         rays, h2d, d2h = n, 104, 13 * n + 32
         api = "render_frame(ProbeGrid, Camera) -> Frame (host arrays)"

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .bake import bake_grid, bake_grid_gpu
-from .grid import ProbeGrid
+from .grid import ProbeGrid, ProbeHierarchy
 from .render import Camera
 from .scenes import city_scene, free_point, room_scene
 
@@ -117,7 +117,7 @@ def c4_levels(seed=404, device=0, levels=C4_LEVELS, r_hi=128, r_lo=32):
 
 def street_cameras(scene, n, width, height, seed, vfov=60.0):
     """Eyes 1.5-12 m above the ground at free points of the block, looking
-    across it with a slight downward pitch."""
+    across it pitched 10-30 degrees down."""
     rng = np.random.default_rng(seed)
     cams = []
     for _ in range(n):
@@ -127,7 +127,7 @@ def street_cameras(scene, n, width, height, seed, vfov=60.0):
             if free_point_ok(scene, eye):
                 break
         yaw = rng.uniform(0.0, 2.0 * np.pi)
-        pitch = np.radians(rng.uniform(-25.0, 0.0))
+        pitch = np.radians(rng.uniform(-30.0, -10.0))
         fwd = (np.cos(pitch) * np.cos(yaw), np.sin(pitch),
                np.cos(pitch) * np.sin(yaw))
         cams.append(Camera(eye=tuple(float(v) for v in eye),
@@ -154,6 +154,7 @@ def c4(seed=404, cam_seed=4404, n_views=1, width=3840, height=2160, device=0):
                  f"128^2/32^2 (f16 payloads), coarse-to-fine; {n_views} view(s) "
                  f"at {width}x{height}")
     cfg.levels = grids
+    cfg.hierarchy = ProbeHierarchy(grids)
     return cfg
 
 

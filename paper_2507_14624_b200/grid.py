@@ -173,3 +173,21 @@ class ProbeGrid:
     def cube_bounds(self, cube):
         lo = self.grid_origin + self.cell_size * np.asarray(cube, dtype=float)
         return lo, lo + self.cell_size
+
+
+class ProbeHierarchy:
+    """Coarse-to-fine stack of probe grids (BASELINE config 4; no reference
+    counterpart): a ray is traced through level 0 and falls through to the
+    next level on MISS (`lfp_render_hierarchy`)."""
+
+    def __init__(self, levels):
+        self.levels = list(levels)
+        if not 1 <= len(self.levels) <= 4:
+            raise ValueError("a hierarchy has 1..4 levels")
+        res = {(g.probe_set.res_hi, g.probe_set.res_lo) for g in self.levels}
+        if len(res) != 1:
+            raise ValueError("all levels must share the map resolutions")
+
+    @property
+    def n_probes(self):
+        return sum(g.probe_set.n_probes for g in self.levels)
