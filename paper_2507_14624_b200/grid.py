@@ -184,9 +184,6 @@ class ProbeHierarchy:
         self.levels = list(levels)
         if not 1 <= len(self.levels) <= 4:
             raise ValueError("a hierarchy has 1..4 levels")
-        res = {(g.probe_set.res_hi, g.probe_set.res_lo) for g in self.levels}
-        if len(res) != 1:
-            raise ValueError("all levels must share the map resolutions")
 
     @property
     def n_probes(self):
