@@ -11,9 +11,12 @@ import __graft_entry__ as g  # noqa: E402
 out = os.path.join(REPO, "build", "variants")
 os.makedirs(out, exist_ok=True)
 srcs = [os.path.join(g.CSRC, "lfp_capi.cu"), os.path.join(g.CSRC, "lfp_bake.cu")]
+# arguments: nested budgets ("4") or persistent budgets ("p3")
 for mb in sys.argv[1:] or ["1", "2", "3", "4", "5"]:
+    macro = "LFP_PERSIST_MIN_BLOCKS" if mb.startswith("p") else "LFP_MIN_BLOCKS"
+    val = mb.lstrip("p")
     lib = os.path.join(out, f"liblfprobe_b200_mb{mb}.so")
-    subprocess.run([g._nvcc(), *g.NVCC_FLAGS, f"-DLFP_MIN_BLOCKS={mb}",
+    subprocess.run([g._nvcc(), *g.NVCC_FLAGS, f"-D{macro}={val}",
                     "-Xptxas", "-v", "-o", lib, *srcs], check=True,
                    stderr=open(lib + ".ptxas.txt", "w"))
     print(lib)
