@@ -280,7 +280,7 @@ __device__ __forceinline__ int lane_transition(Lane& L, int state,
             dg.segs++;
             if (MODE >= 1) L.cf = chord_f(L.c, L.wx, L.wy, L.wz, L.dx, L.dy, L.dz, g.slack);
             else L.cf.ok = false;
-            L.margin = MODE >= 1 ? chord_margin_fast(L.c, R) : chord_margin(L.c, R);
+            L.margin = chord_margin(L.c, R);
             L.lo = dda_init(L.c, ps.r, 0.0, false);
             L.occ_x = L.occ_y = -1;
             state = S_LO;
@@ -332,8 +332,8 @@ __device__ __forceinline__ int lane_lo_step(Lane& L, const DevProbes& ps,
     if (isfinite(m_f)) {
         double s_out = L.lo.t_max_x < L.lo.t_max_y ? L.lo.t_max_x : L.lo.t_max_y;
         if (s_out > 1.0) s_out = 1.0;
-        if (lo_decide<MODE>(L.c, L.cf, m_f, L.lo.s, s_out, L.margin, ps.R, L.wx,
-                            L.wy, L.wz, L.dx, L.dy, L.dz, slack, dg)) {
+        if (lo_decide<MODE>(L.c, L.cf, m_f, L.lo.s, s_out, L.margin, L.wx, L.wy,
+                            L.wz, L.dx, L.dy, L.dz, slack, dg)) {
             L.hi = dda_init(L.c, ps.R, L.lo.s, true);
             L.s_end = s_out;
             L.prev_s = CUDART_NAN;
