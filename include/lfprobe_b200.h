@@ -246,12 +246,6 @@ int lfp_untile(int32_t n_cams, int32_t width, int32_t height, int32_t n_ranks,
                const float* rgb_in, uint8_t* status_out, float* rgb_out,
                void* stream);
 
-/* Diagnostics: ref[i] = a[i] / b[i] (nvcc IEEE division) and shared[i] =
- * the tracer's shared-reciprocal division of the same operands (device
- * arrays); the GPU tests assert they are bit-identical. */
-int lfp_selftest_division(const double* a, const double* b, int64_t n,
-                          double* ref, double* shared, void* stream);
-
 /* ---- input production: GPU ray-cast bake ---- */
 
 /* Analytic primitive: kind 0 = axis-aligned box (a = lo, b = hi), kind 1 =

@@ -118,12 +118,11 @@ def lib():
         L.lfp_trace_rays_ordered.argtypes = [
             vp, ctypes.POINTER(GridParams), vp, vp, i32, i64, vp,
             ctypes.POINTER(Outputs), vp]
-        L.lfp_selftest_division.argtypes = [vp, vp, i64, vp, vp, vp]
         L.lfp_untile.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
         L.lfp_bake_probes.argtypes = [
             ctypes.c_int, ctypes.POINTER(PrimC), i32, ctypes.POINTER(LightC),
             vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-        for name in ("lfp_selftest_division", "lfp_render_hierarchy", "lfp_probeset_create_packed",
+        for name in ("lfp_render_hierarchy", "lfp_probeset_create_packed",
                      "lfp_bin_rays", "lfp_trace_rays_ordered",
                      "lfp_bake_probes", "lfp_render_probes",
                      "lfp_probeset_create", "lfp_probeset_destroy",
@@ -147,5 +146,4 @@ def exported_symbols():
             "lfp_num_tiles", "lfp_render_grid", "lfp_trace_rays",
             "lfp_untile", "lfp_bake_probes", "lfp_render_probes",
             "lfp_bin_rays", "lfp_trace_rays_ordered",
-            "lfp_probeset_create_packed", "lfp_render_hierarchy",
-            "lfp_selftest_division"]
+            "lfp_probeset_create_packed", "lfp_render_hierarchy"]
