@@ -50,7 +50,7 @@ struct Lane {
     double wx, wy, wz, b1, b2, b3;
     // segment (K:373-480)
     Chord c;
-    ChordF cf;
+    ChordF* cf;             // this lane's slot in shared memory
     Dda lo, hi;
     double margin, s_out, s_end, prev_s, prev_r;
     int occ_x, occ_y, hocc_x, hocc_y;
@@ -278,8 +278,8 @@ __device__ __forceinline__ int lane_transition(Lane& L, int state,
             }
             L.c = chord_setup(L.wx, L.wy, L.wz, L.dx, L.dy, L.dz, a, b);
             dg.segs++;
-            if (MODE >= 1) L.cf = chord_f(L.c, L.wx, L.wy, L.wz, L.dx, L.dy, L.dz, g.slack);
-            else L.cf.ok = false;
+            if (MODE >= 1) *L.cf = chord_f(L.c, L.wx, L.wy, L.wz, L.dx, L.dy, L.dz, g.slack);
+            else L.cf->ok = false;
             L.margin = chord_margin(L.c, R);
             L.lo = dda_init(L.c, ps.r, 0.0, false);
             L.occ_x = L.occ_y = -1;
@@ -332,7 +332,7 @@ __device__ __forceinline__ int lane_lo_step(Lane& L, const DevProbes& ps,
     if (isfinite(m_f)) {
         double s_out = L.lo.t_max_x < L.lo.t_max_y ? L.lo.t_max_x : L.lo.t_max_y;
         if (s_out > 1.0) s_out = 1.0;
-        if (lo_decide<MODE>(L.c, L.cf, m_f, L.lo.s, s_out, L.margin, L.wx, L.wy,
+        if (lo_decide<MODE>(L.c, *L.cf, m_f, L.lo.s, s_out, L.margin, L.wx, L.wy,
                             L.wz, L.dx, L.dy, L.dz, slack, dg)) {
             L.hi = dda_init(L.c, ps.R, L.lo.s, true);
             L.s_end = s_out;
@@ -360,7 +360,7 @@ __device__ __forceinline__ int lane_hi_step(Lane& L, const DevProbes& ps,
         if (s_hi > L.s_end) s_hi = L.s_end;
         if (s_hi > 1.0) s_hi = 1.0;
         const double s_lo = L.hi.s > 0.0 ? L.hi.s : 0.0;
-        const int cls = hi_classify<MODE>(ps, L.c, L.cf, stored_f, s_lo, s_hi, ti,
+        const int cls = hi_classify<MODE>(ps, L.c, *L.cf, stored_f, s_lo, s_hi, ti,
                                           L.wx, L.wy, L.wz, L.dx, L.dy, L.dz,
                                           slack, L.prev_s, L.prev_r, dg);
         if (cls == 1) {
