@@ -98,12 +98,14 @@ typedef struct {
     int32_t* fetch;
     float* hit_t;
     unsigned long long* stats;
-    unsigned long long* diag;   /* u64[8]: low-res decisions taken by the
+    unsigned long long* diag;   /* u64[11]: low-res decisions taken by the
                                    filter / by the exact path, hi-res ditto,
                                    filter-vs-exact disagreements (mode 2),
                                    low-res steps cleared by the segment
                                    bound, hi-res texels cleared by the
-                                   squared test, segments traced          */
+                                   squared test, segments traced, fp32-radius
+                                   path outcomes (march, occluder,
+                                   candidate)                             */
     int32_t rgb_mode;
     float background[3];
     float unknown_color[3];

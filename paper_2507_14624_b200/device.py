@@ -143,7 +143,7 @@ class RayOutputs:
         self.fetch = torch.empty(n, dtype=torch.int32, **kw) if fetch else None
         self.hit_t = torch.empty(n, dtype=torch.float32, **kw) if hit_t else None
         self.stats = torch.zeros(4, dtype=torch.int64, **kw) if stats else None
-        self.diag = torch.zeros(8, dtype=torch.int64, **kw) if diag else None
+        self.diag = torch.zeros(11, dtype=torch.int64, **kw) if diag else None
 
     def struct(self, rgb_mode=0, background=(0.0, 0.0, 0.0),
                unknown_color=(1.0, 0.0, 1.0)):

@@ -37,6 +37,7 @@ for mode in ("check", "filtered", "exact"):
     res[mode] = {"ms": e0.elapsed_time(e1), "lo_fast": d[0], "lo_slow": d[1],
                  "hi_fast": d[2], "hi_slow": d[3], "mismatch": d[4],
                  "lo_rseg": d[5], "hi_sq": d[6], "segs": d[7],
+                 "hi_f_cont": d[8], "hi_f_occ": d[9], "hi_f_cand": d[10],
                  "fetch_mean": float(f.mean()),
                  "fetch_p50": float(np.percentile(f, 50)),
                  "fetch_p99": float(np.percentile(f, 99)),
