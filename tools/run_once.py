@@ -18,8 +18,8 @@ from paper_2507_14624_b200.trace import DEFAULT_CONFIG  # noqa: E402
 
 cfg_name, sched = sys.argv[1], sys.argv[2]
 ma = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-if cfg_name == "c2":
-    cfg = configs.c2()
+if cfg_name in ("c2", "c3"):
+    cfg = configs.c2() if cfg_name == "c2" else configs.c3(n_views=1)
     grid = cfg.grid
     cam = cfg.cameras[0]
     n = cam.width * cam.height
@@ -32,13 +32,13 @@ dps = device_probe_set(grid)
 g = dev.grid_params(grid.grid_origin, grid.cell_size, grid.dims, DEFAULT_CONFIG,
                     schedule=sched, min_active=ma)
 out = dev.RayOutputs(n, dps.device, fetch=True)
-if cfg_name != "c2":
+if cfg_name == "c5":
     order = dev.ray_order(dev.bin_rays(g, to, td))
 for _ in range(3):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    if cfg_name == "c2":
+    if cfg_name in ("c2", "c3"):
         dev.render_cameras(dps, g, [cam], cam.width, cam.height, out)
     else:
         dev.trace_rays_ordered(dps, g, to, td, order, out)
