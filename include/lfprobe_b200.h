@@ -278,6 +278,26 @@ int lfp_bake_probes(int device, const lfp_prim* prims_host, int32_t n_prims,
                     int32_t shadows, float* dist_hi, float* dir_hi,
                     float* irr_hi, float* dist_lo, void* stream);
 
+/* ---- the reference's point-cloud bake (bake.py:140-207, grid.py:96-109) ---- */
+
+/* Bake P probes (origins_host f64[P][3]) from one point cloud: positions
+ * f64[n][3] and colors f32[n][3] (PointCloud, pointcloud.py:19-45), host
+ * pointers or, with LFP_SRC_DEVICE, device pointers. Per texel the nearest
+ * point wins (exact-distance ties: smallest (x, y, z, r, g, b),
+ * bake.py:116-137); the maps are the reference's in-memory quantised
+ * values -- RGB565 radiance, float16 distance, 8-bit sub-texel direction
+ * (bake.py:62-91) -- bit-identical to bake_probe, written into caller-owned
+ * DEVICE arrays in the ProbeSet layout (dist_hi f32[P][R][R], dir_hi /
+ * irr_hi f32[P][R][R][3], dist_lo f32[P][r][r] block MIN). skipped_host
+ * (optional, int64[P]) receives the per-probe count of points within 1e-6 of
+ * the origin (bake.py:167-174). n < 2^32 - 1. Synchronous on `stream`.
+ * Replaces bake_probe / simulate_probe / grid.bake_grid's per-probe loop. */
+int lfp_bake_points(int device, const double* positions, const float* colors,
+                    int64_t n_points, const double* origins_host, int64_t P,
+                    int32_t R, int32_t r, uint32_t flags, float* dist_hi,
+                    float* dir_hi, float* irr_hi, float* dist_lo,
+                    int64_t* skipped_host, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -188,6 +188,310 @@ __global__ void block_min_kernel(const float* __restrict__ hi, float* __restrict
     lo[idx] = m;
 }
 
+
+// ---------------------------------------------------------------------------
+// Point-cloud bake (bake.py:140-207, the reference's own bake): every cloud
+// point is projected into every probe's octahedral map; per texel the point
+// with the smallest distance wins, exact-distance ties go to the smallest
+// (x, y, z, r, g, b) (bake.py:116-137), so the result is independent of the
+// point order. Three passes per probe chunk:
+//   1. point_min_kernel: 64-bit atomicMin of the fp64 distance bits (positive
+//      doubles order like their bit patterns) into key[p][texel];
+//   2. point_tie_kernel: points whose distance equals the texel's minimum
+//      race for win[p][texel] with a CAS loop on the lexicographic key (one
+//      candidate per texel unless distances tie exactly);
+//   3. point_finalize_kernel: per texel, the winner's RGB565 radiance,
+//      float16 distance and 8-bit sub-texel direction, decoded exactly as the
+//      reference stores them in memory (bake.py:62-91, 193-198).
+// All arithmetic restates numpy's fp64 op order (no FMA: -fmad=false), so
+// the maps are bit-identical to the reference bake.
+// ---------------------------------------------------------------------------
+
+#ifndef LFP_BAKE_FAST
+#define LFP_BAKE_FAST 1
+#endif
+
+constexpr unsigned kNoWinner = 0xFFFFFFFFu;
+constexpr int kMaxChunkProbes = 64;
+
+// octmap.py:24-43 (numpy op order): l1 = (|x| + |y|) + |z|, fold with
+// sign(0) = +1 using the unfolded px / pz, uv = p * 0.5 + 0.5
+__device__ __forceinline__ void np_oct_encode(double x, double y, double z,
+                                              double& u, double& v)
+{
+    const double l1 = (fabs(x) + fabs(y)) + fabs(z);
+    double px = x / l1;
+    double pz = z / l1;
+    if (y < 0.0) {
+        const double fx = (px >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(pz));
+        const double fz = (pz >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(px));
+        px = fx;
+        pz = fz;
+    }
+    u = px * 0.5 + 0.5;
+    v = pz * 0.5 + 0.5;
+}
+
+// octmap.py:46-64: y = (1 - |fx|) - |fz| is kept unfolded; d /= |d| with
+// |d| = sqrt((x^2 + y^2) + z^2)
+__device__ __forceinline__ void np_oct_decode(double u, double v, float out[3])
+{
+    const double fx = u * 2.0 - 1.0;
+    const double fz = v * 2.0 - 1.0;
+    const double y = (1.0 - fabs(fx)) - fabs(fz);
+    double x = fx, z = fz;
+    if (y < 0.0) {
+        x = (fx >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(fz));
+        z = (fz >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(fx));
+    }
+    const double n = sqrt((x * x + y * y) + z * z);
+    out[0] = (float)(x / n);
+    out[1] = (float)(y / n);
+    out[2] = (float)(z / n);
+}
+
+// bake.py:152-165: w = p - origin, d = |w| (numpy norm order), uv of w / d,
+// texel = min(int(uv * R), R - 1). Returns false for points within 1e-6 of
+// the origin (skipped, bake.py:158-162, 167-174).
+__device__ __forceinline__ bool project_point(const double* __restrict__ pos,
+                                              long long i, const double* o,
+                                              int R, double& d, int& tx,
+                                              int& ty, double& u, double& v)
+{
+    const double wx = pos[3 * i] - o[0];
+    const double wy = pos[3 * i + 1] - o[1];
+    const double wz = pos[3 * i + 2] - o[2];
+    d = sqrt((wx * wx + wy * wy) + wz * wz);
+    if (!(d >= 1e-6)) return false;
+    np_oct_encode(wx / d, wy / d, wz / d, u, v);
+    long long a = (long long)(u * R), b = (long long)(v * R);
+    tx = (int)(a < R - 1 ? a : R - 1);
+    ty = (int)(b < R - 1 ? b : R - 1);
+    return true;
+}
+
+// Texel of w in fp32 with a certainty test (exact-decision filter, as in the
+// tracer): the fp64 chain of project_point and this fp32 chain both
+// approximate U * R (U the exact octahedral coordinate; it does not depend
+// on d) -- fp64 within ~1e-15 R, fp32 within 5 R 2^-24 (six roundings of
+// |p| <= 1 plus the scale; bound used: R * 1e-6, a 3x margin). When u R and
+// v R are farther than that from an integer the floors agree; otherwise (or
+// for components fp32 cannot represent faithfully) return false and let
+// the exact path decide. The fold test (y < 0) and the sign rule use the
+// fp64 signs, which the divisions by d > 0 and l1 > 0 preserve.
+__device__ __forceinline__ bool texel_fast(double wx, double wy, double wz,
+                                           int R, int& tx, int& ty)
+{
+    const float x = (float)wx, y = (float)wy, z = (float)wz;
+    const float ax = fabsf(x), ay = fabsf(y), az = fabsf(z);
+    const float mx = fmaxf(ax, fmaxf(ay, az));
+    if (!(mx > 1e-30f && mx < 1e30f)) return false;
+    const float tiny = 1e-20f * mx;
+    if ((wx != 0.0 && ax < tiny) || (wy != 0.0 && ay < tiny) ||
+        (wz != 0.0 && az < tiny))
+        return false;
+    const float il = __frcp_rn((ax + ay) + az);
+    float px = x * il, pz = z * il;
+    if (wy < 0.0) {
+        const float fx = (px >= 0.0f ? 1.0f : -1.0f) * (1.0f - fabsf(pz));
+        const float fz = (pz >= 0.0f ? 1.0f : -1.0f) * (1.0f - fabsf(px));
+        px = fx;
+        pz = fz;
+    }
+    const float fr = (float)R;
+    const float tu = fmaf(px, 0.5f, 0.5f) * fr;
+    const float tv = fmaf(pz, 0.5f, 0.5f) * fr;
+    const float e = fr * 1e-6f;
+    const float gu = floorf(tu), gv = floorf(tv);
+    const float du = tu - gu, dv = tv - gv;
+    if (!(du > e && du < 1.0f - e && dv > e && dv < 1.0f - e)) return false;
+    tx = (int)gu;
+    ty = (int)gv;
+    return tx >= 0 && tx < R && ty >= 0 && ty < R;
+}
+
+// project_point for the min / tie passes: exact d, texel via texel_fast
+// with the exact fp64 fallback
+__device__ __forceinline__ bool project_texel(const double* __restrict__ pos,
+                                              long long i, const double* o,
+                                              int R, double& d, int& tx,
+                                              int& ty)
+{
+    const double wx = pos[3 * i] - o[0];
+    const double wy = pos[3 * i + 1] - o[1];
+    const double wz = pos[3 * i + 2] - o[2];
+    d = sqrt((wx * wx + wy * wy) + wz * wz);
+    if (!(d >= 1e-6)) return false;
+    if (LFP_BAKE_FAST && texel_fast(wx, wy, wz, R, tx, ty)) return true;
+    double u, v;
+    np_oct_encode(wx / d, wy / d, wz / d, u, v);
+    long long a = (long long)(u * R), b = (long long)(v * R);
+    tx = (int)(a < R - 1 ? a : R - 1);
+    ty = (int)(b < R - 1 ? b : R - 1);
+    return true;
+}
+
+// numpy float64 -> float16 (round to nearest even, straight from the double;
+// bake.py:71-73), returned widened to f32
+__device__ __forceinline__ float f64_to_f16_f32(double x)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const unsigned short sign = (unsigned short)((b >> 48) & 0x8000u);
+    const int ex = (int)((b >> 52) & 0x7FF);
+    const unsigned long long man = b & ((1ull << 52) - 1);
+    unsigned short h;
+    if (ex == 0x7FF) {
+        h = sign | (man ? 0x7E00u : 0x7C00u);
+    } else if (ex == 0) {
+        h = sign;                       // fp64 subnormals underflow to 0
+    } else {
+        const int e = ex - 1023;
+        const unsigned long long m = man | (1ull << 52);
+        if (e > 15) {
+            h = sign | 0x7C00u;
+        } else {
+            int shift = e >= -14 ? 42 : 42 + (-14 - e);
+            unsigned long long q = 0;
+            if (shift < 64) {
+                q = m >> shift;
+                const unsigned long long rem = m & ((1ull << shift) - 1);
+                const unsigned long long half = 1ull << (shift - 1);
+                if (rem > half || (rem == half && (q & 1))) q++;
+            }
+            if (e >= -14) {
+                // q in [1024, 2048]; carry into the exponent is handled by
+                // adding the biased exponent to the full significand
+                const unsigned int bits = ((unsigned)(e + 14) << 10) + (unsigned)q;
+                h = bits >= 0x7C00u ? (sign | 0x7C00u) : (unsigned short)(sign | bits);
+            } else {
+                h = sign | (unsigned short)q;   // q <= 1024 (1024 = min normal)
+            }
+        }
+    }
+    return __half2float(__ushort_as_half(h));
+}
+
+__global__ void point_min_kernel(const double* __restrict__ pos, long long n,
+                                 const double* __restrict__ origins, int np,
+                                 int R, unsigned long long* __restrict__ key,
+                                 unsigned long long* __restrict__ skipped)
+{
+    __shared__ double so[3 * kMaxChunkProbes];
+    __shared__ unsigned s_skip[kMaxChunkProbes];
+    for (int k = threadIdx.x; k < 3 * np; k += blockDim.x) so[k] = origins[k];
+    for (int k = threadIdx.x; k < np; k += blockDim.x) s_skip[k] = 0;
+    __syncthreads();
+    const long long RR = (long long)R * R;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        for (int p = 0; p < np; p++) {
+            double d;
+            int tx, ty;
+            if (!project_texel(pos, i, so + 3 * p, R, d, tx, ty)) {
+                atomicAdd(&s_skip[p], 1u);
+                continue;
+            }
+            atomicMin(key + p * RR + (long long)ty * R + tx,
+                      (unsigned long long)__double_as_longlong(d));
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < np; k += blockDim.x)
+        if (s_skip[k]) atomicAdd(skipped + k, (unsigned long long)s_skip[k]);
+}
+
+// lexicographic (x, y, z, r, g, b, index) order of bake.py:125-137 (numpy
+// lexsort keys, stable on full ties)
+__device__ __forceinline__ bool point_less(const double* __restrict__ pos,
+                                           const float* __restrict__ col,
+                                           unsigned a, unsigned b)
+{
+    for (int k = 0; k < 3; k++) {
+        const double x = pos[3ull * a + k], y = pos[3ull * b + k];
+        if (x < y) return true;
+        if (y < x) return false;
+    }
+    for (int k = 0; k < 3; k++) {
+        const float x = col[3ull * a + k], y = col[3ull * b + k];
+        if (x < y) return true;
+        if (y < x) return false;
+    }
+    return a < b;
+}
+
+__global__ void point_tie_kernel(const double* __restrict__ pos,
+                                 const float* __restrict__ col, long long n,
+                                 const double* __restrict__ origins, int np,
+                                 int R, const unsigned long long* __restrict__ key,
+                                 unsigned* __restrict__ win)
+{
+    __shared__ double so[3 * kMaxChunkProbes];
+    for (int k = threadIdx.x; k < 3 * np; k += blockDim.x) so[k] = origins[k];
+    __syncthreads();
+    const long long RR = (long long)R * R;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        for (int p = 0; p < np; p++) {
+            double d;
+            int tx, ty;
+            if (!project_texel(pos, i, so + 3 * p, R, d, tx, ty)) continue;
+            const long long t = p * RR + (long long)ty * R + tx;
+            if (key[t] != (unsigned long long)__double_as_longlong(d)) continue;
+            const unsigned me = (unsigned)i;
+            unsigned cur = win[t];
+            while (cur == kNoWinner || point_less(pos, col, me, cur)) {
+                const unsigned old = atomicCAS(win + t, cur, me);
+                if (old == cur) break;
+                cur = old;
+            }
+        }
+    }
+}
+
+__global__ void point_finalize_kernel(const double* __restrict__ pos,
+                                      const float* __restrict__ col,
+                                      const double* __restrict__ origins,
+                                      int np, int R,
+                                      const unsigned* __restrict__ win,
+                                      float* __restrict__ dist_hi,
+                                      float* __restrict__ dir_hi,
+                                      float* __restrict__ irr_hi)
+{
+    const long long RR = (long long)R * R;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= np * RR) return;
+    const long long p = idx / RR;
+    const unsigned w = win[idx];
+    float* dd = dir_hi + 3 * idx;
+    float* cc = irr_hi + 3 * idx;
+    if (w == kNoWinner) {
+        dist_hi[idx] = CUDART_INF_F;
+        dd[0] = dd[1] = dd[2] = 0.f;
+        cc[0] = cc[1] = cc[2] = 0.f;
+        return;
+    }
+    double d, u, v;
+    int tx, ty;
+    project_point(pos, w, origins + 3 * p, R, d, tx, ty, u, v);
+    dist_hi[idx] = f64_to_f16_f32(d);
+    // quantize_rgb565 (bake.py:62-68): clip to [0, 1], rint(c * L) / L
+    const double lv[3] = {31.0, 63.0, 31.0};
+    for (int k = 0; k < 3; k++) {
+        double c = (double)col[3ull * w + k];
+        c = c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
+        cc[k] = (float)(rint(c * lv[k]) / lv[k]);
+    }
+    // _quantize_direction / _decode_direction (bake.py:76-91)
+    double fx = u * R - (double)tx;
+    double fy = v * R - (double)ty;
+    double qx = rint(fx * 254.0), qy = rint(fy * 254.0);
+    qx = qx < 0.0 ? 0.0 : (qx > 254.0 ? 254.0 : qx);
+    qy = qy < 0.0 ? 0.0 : (qy > 254.0 ? 254.0 : qy);
+    const double du = ((double)tx + qx / 254.0) / R;
+    const double dv = ((double)ty + qy / 254.0) / R;
+    np_oct_decode(du, dv, dd);
+}
+
 }  // namespace
 
 extern "C" {
@@ -260,4 +564,100 @@ int lfp_bake_probes(int device, const lfp_prim* prims_host, int32_t n_prims,
     return rc;
 }
 
+int lfp_bake_points(int device, const double* positions, const float* colors,
+                    int64_t n_points, const double* origins_host, int64_t P,
+                    int32_t R, int32_t r, uint32_t flags, float* dist_hi,
+                    float* dir_hi, float* irr_hi, float* dist_lo,
+                    int64_t* skipped_host, void* stream)
+{
+    if (!positions || !colors || n_points < 1 || n_points >= 0xFFFFFFFFll ||
+        !origins_host || P < 1 || R < 1 || r < 1 || R % r != 0 || !dist_hi ||
+        !dir_hi || !irr_hi || !dist_lo || R > 32768) {
+        lfp_internal::set_error("lfp_bake_points: invalid arguments");
+        return LFP_ERR_INVALID;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool on_dev = (flags & LFP_SRC_DEVICE) != 0;
+    const long long RR = (long long)R * R;
+    // probe chunk: <= kMaxChunkProbes and <= ~1 GiB of key + winner scratch
+    long long chunk = (1ll << 30) / (12 * RR);
+    if (chunk < 1) chunk = 1;
+    if (chunk > kMaxChunkProbes) chunk = kMaxChunkProbes;
+    if (chunk > P) chunk = P;
+    double* dpos = nullptr;
+    float* dcol = nullptr;
+    double* dorg = nullptr;
+    unsigned long long* key = nullptr;
+    unsigned* win = nullptr;
+    unsigned long long* dskip = nullptr;
+    int rc = LFP_OK;
+    // stream-ordered allocations: the device pool reuses them across calls
+    bool ok = cudaMallocAsync(&dorg, sizeof(double) * 3 * P, st) == cudaSuccess &&
+              cudaMallocAsync(&key, sizeof(unsigned long long) * chunk * RR, st) == cudaSuccess &&
+              cudaMallocAsync(&win, sizeof(unsigned) * chunk * RR, st) == cudaSuccess &&
+              cudaMallocAsync(&dskip, sizeof(unsigned long long) * P, st) == cudaSuccess;
+    if (ok && !on_dev)
+        ok = cudaMallocAsync(&dpos, sizeof(double) * 3 * n_points, st) == cudaSuccess &&
+             cudaMallocAsync(&dcol, sizeof(float) * 3 * n_points, st) == cudaSuccess;
+    if (!ok) {
+        lfp_internal::set_error("lfp_bake_points: cudaMallocAsync failed");
+        rc = LFP_ERR_NOMEM;
+    } else {
+        const double* pos = positions;
+        const float* col = colors;
+        if (!on_dev) {
+            cudaMemcpyAsync(dpos, positions, sizeof(double) * 3 * n_points,
+                            cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(dcol, colors, sizeof(float) * 3 * n_points,
+                            cudaMemcpyHostToDevice, st);
+            pos = dpos;
+            col = dcol;
+        }
+        cudaMemcpyAsync(dorg, origins_host, sizeof(double) * 3 * P,
+                        cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(dskip, 0, sizeof(unsigned long long) * P, st);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const long long want = (n_points + 255) / 256;
+        const unsigned grid = (unsigned)(want < 8ll * sms ? want : 8ll * sms);
+        for (long long p0 = 0; p0 < P; p0 += chunk) {
+            const int np = (int)(P - p0 < chunk ? P - p0 : chunk);
+            cudaMemsetAsync(key, 0xFF, sizeof(unsigned long long) * np * RR, st);
+            cudaMemsetAsync(win, 0xFF, sizeof(unsigned) * np * RR, st);
+            point_min_kernel<<<grid, 256, 0, st>>>(pos, n_points, dorg + 3 * p0,
+                                                   np, R, key, dskip + p0);
+            point_tie_kernel<<<grid, 256, 0, st>>>(pos, col, n_points,
+                                                   dorg + 3 * p0, np, R, key, win);
+            const long long nt = np * RR;
+            point_finalize_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
+                pos, col, dorg + 3 * p0, np, R, win, dist_hi + p0 * RR,
+                dir_hi + 3 * p0 * RR, irr_hi + 3 * p0 * RR);
+        }
+        const long long nl = P * (long long)r * r;
+        block_min_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(
+            dist_hi, dist_lo, P, R, r);
+        if (skipped_host)
+            cudaMemcpyAsync(skipped_host, dskip, sizeof(int64_t) * P,
+                            cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            lfp_internal::set_error(std::string("lfp_bake_points: ") +
+                                    cudaGetErrorString(e));
+            rc = LFP_ERR_CUDA;
+        }
+    }
+    for (void* ptr : {(void*)dpos, (void*)dcol, (void*)dorg, (void*)key,
+                      (void*)win, (void*)dskip})
+        if (ptr) cudaFreeAsync(ptr, st);
+    if (rc != LFP_OK) cudaStreamSynchronize(st);
+    cudaGetLastError();
+    cudaSetDevice(prev);
+    return rc;
+}
+
 }  // extern "C"
+

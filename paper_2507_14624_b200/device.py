@@ -72,6 +72,38 @@ class DeviceProbeSet:
         return self
 
     @classmethod
+    def from_device_tensors(cls, dist_hi, dir_hi, irr_hi, dist_lo, origins,
+                            device=0, half="auto", stream=None):
+        """Create from maps already on the device (torch tensors in the
+        ProbeSet layout, e.g. the GPU bake's output): LFP_SRC_DEVICE, no
+        host round trip. `origins` may be host (numpy) or device."""
+        dvc = _require_cuda(device)
+        ts = [t.contiguous() for t in (dist_hi, dir_hi, irr_hi, dist_lo)]
+        if any(t.dtype != torch.float32 or t.device != dvc for t in ts):
+            raise ValueError("device maps must be float32 tensors on "
+                             f"{dvc}")
+        org = np.ascontiguousarray(np.asarray(origins, np.float64)) if not \
+            isinstance(origins, torch.Tensor) else origins.contiguous()
+        P, R, R2 = ts[0].shape
+        r = ts[3].shape[1]
+        if R != R2 or tuple(ts[1].shape) != (P, R, R, 3) or tuple(
+                ts[2].shape) != (P, R, R, 3) or tuple(ts[3].shape) != (P, r, r) \
+                or tuple(org.shape) != (P, 3):
+            raise ValueError("probe set arrays have inconsistent shapes")
+        flags = native.LFP_SRC_DEVICE | {
+            "auto": native.LFP_FMT_AUTO_HALF,
+            "never": native.LFP_FMT_FORCE_F32}[half]
+        optr = (ctypes.c_void_p(org.data_ptr()) if isinstance(org, torch.Tensor)
+                else org.ctypes.data_as(ctypes.c_void_p))
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(dvc):
+            st = stream if stream is not None else torch.cuda.current_stream(dvc)
+            native.check(native.lib().lfp_probeset_create(
+                dvc.index, *[_ptr(t) for t in ts], optr, P, R, r, flags,
+                ctypes.c_void_p(st.cuda_stream), ctypes.byref(handle)))
+        return cls.from_handle(handle, dvc, P, R, r)
+
+    @classmethod
     def from_probe_set(cls, ps, device=0, half="auto"):
         return cls(ps.dist_hi, ps.dir_hi, ps.irr_hi, ps.dist_lo, ps.origins,
                    device=device, half=half)

@@ -57,13 +57,15 @@ class MapChain:
 
 @dataclass(frozen=True)
 class ProbeData:
-    """One probe: origin, map chain, bounds (`bake.py:45-59`)."""
+    """One probe: origin, map chain, bake metadata (`bake.py:45-59`)."""
 
     origin: np.ndarray
     chain: MapChain
     bounds_lo: np.ndarray = None
     bounds_hi: np.ndarray = None
     source: str = ""
+    point_count: int = 0
+    timestamp: float = 0.0
 
     def __post_init__(self):
         object.__setattr__(self, "origin",

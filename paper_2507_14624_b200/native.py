@@ -122,7 +122,10 @@ def lib():
         L.lfp_bake_probes.argtypes = [
             ctypes.c_int, ctypes.POINTER(PrimC), i32, ctypes.POINTER(LightC),
             vp, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
-        for name in ("lfp_render_hierarchy", "lfp_probeset_create_packed",
+        L.lfp_bake_points.argtypes = [
+            ctypes.c_int, vp, vp, i64, vp, i64, i32, i32, u32, vp, vp, vp, vp,
+            vp, vp]
+        for name in ("lfp_bake_points", "lfp_render_hierarchy", "lfp_probeset_create_packed",
                      "lfp_bin_rays", "lfp_trace_rays_ordered",
                      "lfp_bake_probes", "lfp_render_probes",
                      "lfp_probeset_create", "lfp_probeset_destroy",
@@ -146,4 +149,5 @@ def exported_symbols():
             "lfp_num_tiles", "lfp_render_grid", "lfp_trace_rays",
             "lfp_untile", "lfp_bake_probes", "lfp_render_probes",
             "lfp_bin_rays", "lfp_trace_rays_ordered",
-            "lfp_probeset_create_packed", "lfp_render_hierarchy"]
+            "lfp_probeset_create_packed", "lfp_render_hierarchy",
+            "lfp_bake_points"]

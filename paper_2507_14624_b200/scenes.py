@@ -270,3 +270,40 @@ def free_point(scene, rng, margin=0.3, tries=1000):
         if ok:
             return p
     raise RuntimeError("no free camera position found")
+
+
+def sample_point_cloud(scene, density, seed=0):
+    """Seeded surface sampling at ~`density` points per m^2 (input
+    production for the point-cloud bake, in the spirit of the reference's
+    `scenes.py:200-251`): every box face gets round(density * area) uniform
+    points, every sphere round(density * 4 pi r^2) Gaussian-normalised
+    points; colour = the primitive's albedo. Each primitive draws from its
+    own stream default_rng([seed, i]). Returns a PointCloud."""
+    from .pointcloud import PointCloud
+
+    if density <= 0:
+        raise ValueError("density must be positive")
+    pts, cols = [], []
+    for i, prim in enumerate(scene.primitives):
+        rng = np.random.default_rng([seed, i])
+        if isinstance(prim, Box):
+            lo = np.asarray(prim.lo, np.float64)
+            hi = np.asarray(prim.hi, np.float64)
+            ext = hi - lo
+            for ax in range(3):
+                a, b = (ax + 1) % 3, (ax + 2) % 3
+                n = int(round(density * ext[a] * ext[b]))
+                for side in (lo[ax], hi[ax]):
+                    p = np.empty((n, 3))
+                    p[:, ax] = side
+                    p[:, a] = lo[a] + rng.random(n) * ext[a]
+                    p[:, b] = lo[b] + rng.random(n) * ext[b]
+                    pts.append(p)
+                    cols.append(np.broadcast_to(prim.albedo, (n, 3)))
+        else:
+            n = int(round(density * 4.0 * np.pi * prim.radius ** 2))
+            v = rng.normal(size=(n, 3))
+            v /= np.linalg.norm(v, axis=-1, keepdims=True)
+            pts.append(np.asarray(prim.center) + prim.radius * v)
+            cols.append(np.broadcast_to(prim.albedo, (n, 3)))
+    return PointCloud(np.concatenate(pts), np.concatenate(cols).astype(np.float32))

@@ -14,9 +14,9 @@ srcs = [os.path.join(g.CSRC, "lfp_capi.cu"), os.path.join(g.CSRC, "lfp_bake.cu")
 # arguments: nested budgets ("4") or persistent budgets ("p3")
 for mb in sys.argv[1:] or ["1", "2", "3", "4", "5"]:
     macro = {"p": "LFP_PERSIST_MIN_BLOCKS", "s": "LFP_MERGED_SEGMENT",
-             "c": "LFP_CF_SMEM", "h": "LFP_MIN_BLOCKS_HI_RES"}.get(
-        mb[0], "LFP_MIN_BLOCKS")
-    val = mb.lstrip("psch")
+             "c": "LFP_CF_SMEM", "h": "LFP_MIN_BLOCKS_HI_RES",
+             "b": "LFP_BAKE_FAST"}.get(mb[0], "LFP_MIN_BLOCKS")
+    val = mb.lstrip("pschb")
     lib = os.path.join(out, f"liblfprobe_b200_mb{mb}.so")
     subprocess.run([g._nvcc(), *g.NVCC_FLAGS, f"-D{macro}={val}",
                     "-Xptxas", "-v", "-o", lib, *srcs], check=True,
