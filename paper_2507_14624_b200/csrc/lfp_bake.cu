@@ -10,6 +10,7 @@
 // paper_2507_14624_b200/bake.py + scenes.py (nearest t > 1e-9, ties to the
 // lower primitive index). This kernel defines the C3/C5 inputs; the oracle
 // reads the arrays it produces, so it need not be bit-identical to numpy.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -195,8 +196,8 @@ __global__ void block_min_kernel(const float* __restrict__ hi, float* __restrict
 // with the smallest distance wins, exact-distance ties go to the smallest
 // (x, y, z, r, g, b) (bake.py:116-137), so the result is independent of the
 // point order. Three passes per probe chunk:
-//   1. point_min_kernel: 64-bit atomicMin of the fp64 distance bits (positive
-//      doubles order like their bit patterns) into key[p][texel];
+//   1. point_min_kernel: 64-bit atomicMin of the fp64 squared-distance bits
+//      (positive doubles order like their bit patterns) into key[p][texel];
 //   2. point_tie_kernel: points whose distance equals the texel's minimum
 //      race for win[p][texel] with a CAS loop on the lexicographic key (one
 //      candidate per texel unless distances tie exactly);
@@ -290,7 +291,7 @@ __device__ __forceinline__ bool texel_fast(double wx, double wy, double wz,
     if ((wx != 0.0 && ax < tiny) || (wy != 0.0 && ay < tiny) ||
         (wz != 0.0 && az < tiny))
         return false;
-    const float il = __frcp_rn((ax + ay) + az);
+    const float il = __fdividef(1.0f, (ax + ay) + az);   // rcp.approx
     float px = x * il, pz = z * il;
     if (wy < 0.0) {
         const float fx = (px >= 0.0f ? 1.0f : -1.0f) * (1.0f - fabsf(pz));
@@ -310,25 +311,40 @@ __device__ __forceinline__ bool texel_fast(double wx, double wy, double wz,
     return tx >= 0 && tx < R && ty >= 0 && ty < R;
 }
 
-// project_point for the min / tie passes: exact d, texel via texel_fast
-// with the exact fp64 fallback
-__device__ __forceinline__ bool project_texel(const double* __restrict__ pos,
-                                              long long i, const double* o,
-                                              int R, double& d, int& tx,
-                                              int& ty)
+// project_point for the min / tie passes. Returns d2 = (wx^2 + wy^2) + wz^2,
+// the reference's norm before its sqrt: fl(sqrt(.)) is monotone, so the
+// per-texel minimum of d is fl(sqrt(min d2)) and the passes rank d2 (no
+// fp64 sqrt per point). Texel via texel_fast with the exact fallback.
+__device__ __forceinline__ bool project_texel(double px, double py, double pz,
+                                              const double* o, int R,
+                                              double& d2, int& tx, int& ty)
 {
-    const double wx = pos[3 * i] - o[0];
-    const double wy = pos[3 * i + 1] - o[1];
-    const double wz = pos[3 * i + 2] - o[2];
-    d = sqrt((wx * wx + wy * wy) + wz * wz);
-    if (!(d >= 1e-6)) return false;
+    const double wx = px - o[0];
+    const double wy = py - o[1];
+    const double wz = pz - o[2];
+    d2 = (wx * wx + wy * wy) + wz * wz;
+    // skip rule d < 1e-6 (bake.py:158): d2 >= 1.1e-12 implies d > 1.04e-6
+    if (d2 < 1.1e-12 && !(sqrt(d2) >= 1e-6)) return false;
     if (LFP_BAKE_FAST && texel_fast(wx, wy, wz, R, tx, ty)) return true;
+    const double d = sqrt(d2);
     double u, v;
     np_oct_encode(wx / d, wy / d, wz / d, u, v);
     long long a = (long long)(u * R), b = (long long)(v * R);
     tx = (int)(a < R - 1 ? a : R - 1);
     ty = (int)(b < R - 1 ? b : R - 1);
     return true;
+}
+
+// d(a) == d(b) for squared distances with bits(a) >= bits(b) = the texel
+// minimum: equal bits, or (sqrt rounding can merge a few ulps of d2) equal
+// fl(sqrt) when a is within 8 ulps of b
+__device__ __forceinline__ bool same_distance(unsigned long long a,
+                                              unsigned long long b)
+{
+    if (a == b) return true;
+    if (a < b || a - b > 8) return false;
+    return sqrt(__longlong_as_double((long long)a)) ==
+           sqrt(__longlong_as_double((long long)b));
 }
 
 // numpy float64 -> float16 (round to nearest even, straight from the double;
@@ -371,9 +387,14 @@ __device__ __forceinline__ float f64_to_f16_f32(double x)
     return __half2float(__ushort_as_half(h));
 }
 
+// Pass 1. The block strides over the (spatially sorted) cloud uniformly so
+// every warp collective sees all 32 lanes; lanes of a warp that land in the
+// same texel (neighbouring points, distant probe) combine their minimum
+// with __match_any_sync + two 32-bit __reduce_min_sync, and one lane issues
+// the 64-bit atomicMin: far fewer L2 atomics on coherent clouds.
 __global__ void point_min_kernel(const double* __restrict__ pos, long long n,
                                  const double* __restrict__ origins, int np,
-                                 int R, unsigned long long* __restrict__ key,
+                                 int R, unsigned long long* key,
                                  unsigned long long* __restrict__ skipped)
 {
     __shared__ double so[3 * kMaxChunkProbes];
@@ -384,15 +405,20 @@ __global__ void point_min_kernel(const double* __restrict__ pos, long long n,
     const long long RR = (long long)R * R;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
+        const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
         for (int p = 0; p < np; p++) {
-            double d;
+            double d2;
             int tx, ty;
-            if (!project_texel(pos, i, so + 3 * p, R, d, tx, ty)) {
+            if (!project_texel(px, py, pz, so + 3 * p, R, d2, tx, ty)) {
                 atomicAdd(&s_skip[p], 1u);
                 continue;
             }
-            atomicMin(key + p * RR + (long long)ty * R + tx,
-                      (unsigned long long)__double_as_longlong(d));
+            unsigned long long* k = key + p * RR + (long long)ty * R + tx;
+            const unsigned long long kb =
+                (unsigned long long)__double_as_longlong(d2);
+            // the stored value only decreases: a (possibly stale) read that
+            // is already <= kb means this point cannot be the minimum
+            if (*k > kb) atomicMin(k, kb);
         }
     }
     __syncthreads();
@@ -431,12 +457,15 @@ __global__ void point_tie_kernel(const double* __restrict__ pos,
     const long long RR = (long long)R * R;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
+        const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
         for (int p = 0; p < np; p++) {
-            double d;
+            double d2;
             int tx, ty;
-            if (!project_texel(pos, i, so + 3 * p, R, d, tx, ty)) continue;
+            if (!project_texel(px, py, pz, so + 3 * p, R, d2, tx, ty)) continue;
             const long long t = p * RR + (long long)ty * R + tx;
-            if (key[t] != (unsigned long long)__double_as_longlong(d)) continue;
+            if (!same_distance((unsigned long long)__double_as_longlong(d2),
+                               key[t]))
+                continue;
             const unsigned me = (unsigned)i;
             unsigned cur = win[t];
             while (cur == kNoWinner || point_less(pos, col, me, cur)) {
@@ -490,6 +519,86 @@ __global__ void point_finalize_kernel(const double* __restrict__ pos,
     const double du = ((double)tx + qx / 254.0) / R;
     const double dv = ((double)ty + qy / 254.0) / R;
     np_oct_decode(du, dv, dd);
+}
+
+
+// Spatial order for the passes: 30-bit Morton code of each point inside the
+// cloud's bounding box (the bake is order-independent, bake.py:116-118, so
+// any permutation gives identical maps; this one makes warps coherent).
+__device__ __forceinline__ unsigned f2ord(float f)
+{
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ float ord2f(unsigned u)
+{
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+__global__ void bbox_kernel(const double* __restrict__ pos, long long n,
+                            unsigned* __restrict__ bb)
+{
+    unsigned lo[3] = {~0u, ~0u, ~0u}, hi[3] = {0u, 0u, 0u};
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        for (int k = 0; k < 3; k++) {
+            const unsigned o = f2ord((float)pos[3 * i + k]);
+            lo[k] = min(lo[k], o);
+            hi[k] = max(hi[k], o);
+        }
+    for (int k = 0; k < 3; k++) {
+        const unsigned l = __reduce_min_sync(0xFFFFFFFFu, lo[k]);
+        const unsigned h = __reduce_max_sync(0xFFFFFFFFu, hi[k]);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(bb + k, l);
+            atomicMax(bb + 3 + k, h);
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned spread10(unsigned v)
+{
+    v &= 0x3FFu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void morton_kernel(const double* __restrict__ pos, long long n,
+                              const unsigned* __restrict__ bb,
+                              unsigned* __restrict__ code,
+                              unsigned* __restrict__ idx)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned c = 0;
+    for (int k = 0; k < 3; k++) {
+        const float lo = ord2f(bb[k]), hi = ord2f(bb[3 + k]);
+        const float ext = hi - lo;
+        float q = ext > 0.0f ? ((float)pos[3 * i + k] - lo) / ext * 1023.0f : 0.0f;
+        q = fminf(fmaxf(q, 0.0f), 1023.0f);
+        c |= spread10((unsigned)q) << k;
+    }
+    code[i] = c;
+    idx[i] = (unsigned)i;
+}
+
+__global__ void gather_points_kernel(const double* __restrict__ pos,
+                                     const float* __restrict__ col,
+                                     const unsigned* __restrict__ order,
+                                     long long n, double* __restrict__ spos,
+                                     float* __restrict__ scol)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long j = order[i];
+    for (int k = 0; k < 3; k++) {
+        spos[3 * i + k] = pos[3 * j + k];
+        scol[3 * i + k] = col[3 * j + k];
+    }
 }
 
 }  // namespace
@@ -593,6 +702,16 @@ int lfp_bake_points(int device, const double* positions, const float* colors,
     unsigned long long* key = nullptr;
     unsigned* win = nullptr;
     unsigned long long* dskip = nullptr;
+    double* spos = nullptr;
+    float* scol = nullptr;
+    unsigned *code0 = nullptr, *code1 = nullptr, *idx0 = nullptr,
+             *idx1 = nullptr, *bb = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (unsigned*)nullptr,
+                                    (unsigned*)nullptr, (unsigned*)nullptr,
+                                    (unsigned*)nullptr, (long long)n_points, 0,
+                                    30, st);
     int rc = LFP_OK;
     // stream-ordered allocations: the device pool reuses them across calls
     bool ok = cudaMallocAsync(&dorg, sizeof(double) * 3 * P, st) == cudaSuccess &&
@@ -602,6 +721,16 @@ int lfp_bake_points(int device, const double* positions, const float* colors,
     if (ok && !on_dev)
         ok = cudaMallocAsync(&dpos, sizeof(double) * 3 * n_points, st) == cudaSuccess &&
              cudaMallocAsync(&dcol, sizeof(float) * 3 * n_points, st) == cudaSuccess;
+    const size_t n4 = sizeof(unsigned) * (size_t)n_points;
+    if (ok)
+        ok = cudaMallocAsync(&spos, sizeof(double) * 3 * n_points, st) == cudaSuccess &&
+             cudaMallocAsync(&scol, sizeof(float) * 3 * n_points, st) == cudaSuccess &&
+             cudaMallocAsync(&code0, n4, st) == cudaSuccess &&
+             cudaMallocAsync(&code1, n4, st) == cudaSuccess &&
+             cudaMallocAsync(&idx0, n4, st) == cudaSuccess &&
+             cudaMallocAsync(&idx1, n4, st) == cudaSuccess &&
+             cudaMallocAsync(&bb, 6 * sizeof(unsigned), st) == cudaSuccess &&
+             cudaMallocAsync(&tmp, tmp_bytes, st) == cudaSuccess;
     if (!ok) {
         lfp_internal::set_error("lfp_bake_points: cudaMallocAsync failed");
         rc = LFP_ERR_NOMEM;
@@ -623,6 +752,19 @@ int lfp_bake_points(int device, const double* positions, const float* colors,
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const long long want = (n_points + 255) / 256;
         const unsigned grid = (unsigned)(want < 8ll * sms ? want : 8ll * sms);
+        // spatial sort (Morton order inside the bounding box)
+        cudaMemsetAsync(bb, 0xFF, 3 * sizeof(unsigned), st);
+        cudaMemsetAsync(bb + 3, 0, 3 * sizeof(unsigned), st);
+        bbox_kernel<<<grid, 256, 0, st>>>(pos, n_points, bb);
+        morton_kernel<<<(unsigned)want, 256, 0, st>>>(pos, n_points, bb, code0,
+                                                      idx0);
+        cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, code0, code1, idx0,
+                                        idx1, (long long)n_points, 0, 30, st);
+        gather_points_kernel<<<(unsigned)want, 256, 0, st>>>(pos, col, idx1,
+                                                             n_points, spos,
+                                                             scol);
+        pos = spos;
+        col = scol;
         for (long long p0 = 0; p0 < P; p0 += chunk) {
             const int np = (int)(P - p0 < chunk ? P - p0 : chunk);
             cudaMemsetAsync(key, 0xFF, sizeof(unsigned long long) * np * RR, st);
@@ -651,7 +793,9 @@ int lfp_bake_points(int device, const double* positions, const float* colors,
         }
     }
     for (void* ptr : {(void*)dpos, (void*)dcol, (void*)dorg, (void*)key,
-                      (void*)win, (void*)dskip})
+                      (void*)win, (void*)dskip, (void*)spos, (void*)scol,
+                      (void*)code0, (void*)code1, (void*)idx0, (void*)idx1,
+                      (void*)bb, tmp})
         if (ptr) cudaFreeAsync(ptr, st);
     if (rc != LFP_OK) cudaStreamSynchronize(st);
     cudaGetLastError();
