@@ -464,12 +464,15 @@ def e2e_measure(wl, steps, world, rank, local):
 
     import paper_2507_14624_b200 as pkg
     if wl.name == "c5":
-        n = min(wl.n_local, 1 << 22)
+        n = wl.n_local                       # this rank's whole share
         o_h = wl.o[:n].cpu().numpy()
         d_h = wl.d[:n].cpu().numpy()
-        pkg.trace_rays(wl.cfg.grid, o_h, d_h, device=local)
         call = lambda: pkg.trace_rays(wl.cfg.grid, o_h, d_h, device=local)  # noqa: E731
-        rays, h2d, d2h = n, 24 * n, 13 * n + 32
+        r = call()
+        d2h = sum(a.nbytes for a in (r.status, r.probe, r.tx, r.ty, r.fetch,
+                                     r.rgb, r.hit_t, r.stats))
+        del r
+        rays, h2d = n, o_h.nbytes + d_h.nbytes
         api = "trace_rays(ProbeGrid, origins, dirs) host f32 arrays -> host results"
     else:
         cam = wl.cams[rank % len(wl.cams)]

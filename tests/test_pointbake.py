@@ -10,9 +10,10 @@ import numpy as np
 import pytest
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, os.path.join(REPO, "oracle"))
+if REPO not in sys.path:
+    sys.path.insert(0, REPO)
 
-import bake_oracle  # noqa: E402  (test infrastructure)
+from oracle import bake_oracle  # noqa: E402  (test infrastructure)
 
 MAPS = ("irradiance_hi", "distance_hi", "direction_hi", "distance_lo",
         "direction_lo")
@@ -212,8 +213,7 @@ def test_gpu_baked_grid_renders_like_oracle():
     """bake_grid leaves the probe set resident; render_frame on it equals
     the C oracle traced over the same (GPU-baked) maps."""
     _gpu()
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import oracle
+    from oracle import oracle
     from paper_2507_14624_b200 import pointbake, scenes
     from paper_2507_14624_b200.render import Camera, render_frame
     c = scenes.sample_point_cloud(scenes.room_scene(11), 400.0, seed=2)

@@ -89,8 +89,7 @@ def main():
 
     cpu = None
     if not a.no_cpu:
-        sys.path.insert(0, os.path.join(REPO, "oracle"))
-        import bake_oracle
+        from oracle import bake_oracle
         n = min(N, a.cpu_points)
         sel = np.random.default_rng(0).choice(N, n, replace=False)
         t0 = time.perf_counter()
