@@ -89,7 +89,10 @@ typedef struct {
  *  stats  u64[4]     accumulated: {sum fetch, #MISS, #UNKNOWN, #HIT}
  * rgb_mode 0 = frame fill (render.py:147-149): HIT radiance, MISS
  * `background`, UNKNOWN `unknown_color`; rgb_mode 1 = kernel semantics
- * (kernels.py:840-843): only HIT rows are written. */
+ * (kernels.py:840-843): only HIT rows are written.
+ *  rgb8   u8[n*3]    (optional) the frame-filled colour as Frame.rgb8
+ *                    (render.py:70-73): clip(rint(c * 255), 0, 255) --
+ *                    what the service PNG-encodes (service.py:101-104) */
 typedef struct {
     uint8_t* status;
     float* rgb;
@@ -109,6 +112,7 @@ typedef struct {
     int32_t rgb_mode;
     float background[3];
     float unknown_color[3];
+    uint8_t* rgb8;
 } lfp_outputs;
 
 /* Library version (major*10000 + minor*100 + patch). */

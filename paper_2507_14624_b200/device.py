@@ -180,7 +180,7 @@ class RayOutputs:
 
     def __init__(self, n, device, status=True, rgb=True, probe=False,
                  texel=False, fetch=False, hit_t=False, stats=True,
-                 diag=False):
+                 diag=False, rgb8=False):
         kw = dict(device=device)
         self.n = n
         self.status = torch.empty(n, dtype=torch.uint8, **kw) if status else None
@@ -191,6 +191,7 @@ class RayOutputs:
         self.hit_t = torch.empty(n, dtype=torch.float32, **kw) if hit_t else None
         self.stats = torch.zeros(4, dtype=torch.int64, **kw) if stats else None
         self.diag = torch.zeros(11, dtype=torch.int64, **kw) if diag else None
+        self.rgb8 = torch.empty((n, 3), dtype=torch.uint8, **kw) if rgb8 else None
 
     def struct(self, rgb_mode=0, background=(0.0, 0.0, 0.0),
                unknown_color=(1.0, 0.0, 1.0)):
@@ -203,6 +204,7 @@ class RayOutputs:
         o.hit_t = _ptr(self.hit_t)
         o.stats = _ptr(self.stats)
         o.diag = _ptr(self.diag)
+        o.rgb8 = _ptr(self.rgb8)
         o.rgb_mode = int(rgb_mode)
         for k in range(3):
             o.background[k] = float(background[k])

@@ -122,6 +122,18 @@ class ProbeSet:
         return self.dist_lo.shape[1]
 
     @property
+    def bounds(self):
+        """Union of the probes' bake bounds (`grid.py:41-45`); probe sets
+        built from bare arrays fall back to the origins' box."""
+        probes = self.probes or []
+        if probes and all(getattr(p, "bounds_lo", None) is not None
+                          for p in probes):
+            lo = np.min([p.bounds_lo for p in probes], axis=0)
+            hi = np.max([p.bounds_hi for p in probes], axis=0)
+            return lo, hi
+        return self.origins.min(axis=0), self.origins.max(axis=0)
+
+    @property
     def nbytes(self):
         return sum(a.nbytes for a in (self.dist_hi, self.dir_hi, self.irr_hi,
                                       self.dist_lo, self.origins))
@@ -175,6 +187,10 @@ class ProbeGrid:
     def cube_bounds(self, cube):
         lo = self.grid_origin + self.cell_size * np.asarray(cube, dtype=float)
         return lo, lo + self.cell_size
+
+    @property
+    def bounds(self):
+        return self.probe_set.bounds
 
 
 class ProbeHierarchy:

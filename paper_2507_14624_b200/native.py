@@ -65,7 +65,8 @@ class Outputs(ctypes.Structure):
                 ("diag", ctypes.c_void_p),
                 ("rgb_mode", ctypes.c_int32),
                 ("background", ctypes.c_float * 3),
-                ("unknown_color", ctypes.c_float * 3)]
+                ("unknown_color", ctypes.c_float * 3),
+                ("rgb8", ctypes.c_void_p)]
 
 
 _lib = None
