@@ -329,6 +329,8 @@ class Workload:
                                  min_active=args.min_active)
         self.stream = torch.cuda.current_stream(dvc)
         self.extra_in_bytes = 0
+        self.launches = 1          # our kernels per trace() call
+        self.binned = False
         if name == "c5":
             from paper_2507_14624_b200 import configs
             lo = rank * C5_RAYS // world
@@ -344,7 +346,10 @@ class Workload:
             self.extra_in_bytes = 24
             self.rays_per_step = C5_RAYS
             self.frames_per_step = 0
-            self.binned = not args.no_binning
+            # the wavefront schedule (default at this size) sorts its rays
+            # itself; binning applies to the per-ray schedules
+            self.binned = (not args.no_binning and
+                           args.schedule in ("nested", "persistent"))
         else:
             cams = self.cfg.cameras
             self.cams = cams
@@ -378,6 +383,7 @@ class Workload:
             else:
                 dev.trace_rays(self.dps, self.g, self.o, self.d, self.out,
                                stream=self.stream)
+            self.launches = dev.last_launches()
             return
         if self.levels is not None:
             if self.world == 1:
@@ -420,8 +426,9 @@ class Workload:
 
     def launches_per_step(self):
         if self.name == "c5":
-            # bin keys + sort (library) + ordered trace; only ours counted
-            return 2 if self.binned else 1
+            # bin keys + sort (library) + ordered trace, or the wavefront's
+            # iterations (CUB sorts not counted); only ours counted
+            return (1 if self.binned else 0) + self.launches
         return 1 + (1 if (self.world > 1 and self.rank == 0) else 0)
 
     def algorithmic_bytes(self):
@@ -520,7 +527,7 @@ def main():
                     help="trace_mode: fp32 decision filters + exact fallback "
                          "(default), exact fp64 only, or self-check")
     ap.add_argument("--schedule", default="default",
-                    choices=["default", "nested", "persistent"],
+                    choices=["default", "nested", "persistent", "wave"],
                     help="traversal schedule (default: nested for cameras, "
                          "persistent for explicit rays)")
     ap.add_argument("--min-active", type=int, default=0,
@@ -602,7 +609,11 @@ def main():
         cpu = cpu_baseline(wl.cfg, args.config, args.cpu_budget)
 
     if rank == 0:
-        kernel = {"c5": "trace_rays_kernel (binned)",
+        kernel = {"c5": ("wave_kernel: all wavefront iterations of the step "
+                         "incl. the CUB sorts between them"
+                         if wl.launches > 1 else
+                         "trace_rays_kernel / persistent_kernel" +
+                         (" (binned)" if wl.binned else "")),
                   "c4": "render_hierarchy_kernel"}.get(args.config,
                                                        "render_cameras_kernel")
         line = {

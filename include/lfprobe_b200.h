@@ -60,11 +60,15 @@ typedef struct {
                                the reference; 1 = exact fp64 on every step;
                                2 = filtered + re-check of every filtered
                                decision (counts into lfp_outputs.diag)    */
-    int32_t schedule;       /* 0 = entry point default (cameras: nested,
-                               explicit rays: persistent); 1 = nested: one
-                               thread per ray; 2 = persistent: flattened
-                               per-lane state machine, lanes pull rays from
-                               a global counter                           */
+    int32_t schedule;       /* 0 = entry point default (cameras: nested;
+                               explicit rays: wavefront from 2^20 rays,
+                               persistent below); 1 = nested: one thread
+                               per ray; 2 = persistent: flattened per-lane
+                               state machine, lanes pull rays from a global
+                               counter; 3 = wavefront (explicit rays): one
+                               probe trace per ray per launch, rays
+                               re-sorted by (probe, chord ends) between
+                               launches; blocks the calling thread        */
     int32_t min_active;     /* persistent: keep stepping while >= this many
                                lanes of a warp step (1..32, 0 = 16)      */
 } lfp_grid_params;
@@ -120,6 +124,11 @@ int lfp_version(void);
 
 /* Thread-local message of the last failing call on this thread. */
 const char* lfp_last_error(void);
+
+/* Kernels launched by this thread's last lfp_trace_rays /
+ * lfp_trace_rays_ordered / lfp_render_grid call (the wavefront schedule
+ * launches one per iteration; the others one). */
+int64_t lfp_last_launches(void);
 
 /* Upload + relayout a ProbeSet (grid.py:19-45 arrays):
  *   dist_hi f32[P][R][R], dir_hi f32[P][R][R][3], irr_hi f32[P][R][R][3],

@@ -58,19 +58,20 @@ struct Lane {
     int status, rp, rtx, rty;
 };
 
-// K:653-738: lattice entry of the lane's ray; returns false for a ray that
-// misses the lattice (MISS, 0 fetches).
-__device__ __forceinline__ bool lane_ray_init(Lane& L, const GridParams& g)
+// K:668-692: slab test of the ray against the lattice AABB; false when the
+// ray misses it (or the lattice is degenerate, G:118-120).
+__device__ __forceinline__ bool lattice_slab(const GridParams& g, double ex,
+                                             double ey, double ez, double dx,
+                                             double dy, double dz,
+                                             double& t_near_out,
+                                             double& t_far_out)
 {
-    L.fetches = 0;
-    L.best_p = L.best_tx = L.best_ty = -1;
-    L.status = MISS; L.rp = -1; L.rtx = -1; L.rty = -1;
     const int cx = g.nx - 1, cy = g.ny - 1, cz = g.nz - 1;
     if (cx < 1 || cy < 1 || cz < 1) return false;
     const double cell = g.cell;
     double t_near = -CUDART_INF, t_far = CUDART_INF;
-    const double oo[3] = {L.ex, L.ey, L.ez};
-    const double dd[3] = {L.dx, L.dy, L.dz};
+    const double oo[3] = {ex, ey, ez};
+    const double dd[3] = {dx, dy, dz};
     const double hi3[3] = {g.g0[0] + (double)cx * cell, g.g0[1] + (double)cy * cell,
                            g.g0[2] + (double)cz * cell};
 #pragma unroll
@@ -88,6 +89,23 @@ __device__ __forceinline__ bool lane_ray_init(Lane& L, const GridParams& g)
         }
     }
     if (t_far < t_near || t_far <= 0.0) return false;
+    t_near_out = t_near;
+    t_far_out = t_far;
+    return true;
+}
+
+// K:653-738: lattice entry of the lane's ray; returns false for a ray that
+// misses the lattice (MISS, 0 fetches).
+__device__ __forceinline__ bool lane_ray_init(Lane& L, const GridParams& g)
+{
+    L.fetches = 0;
+    L.best_p = L.best_tx = L.best_ty = -1;
+    L.status = MISS; L.rp = -1; L.rtx = -1; L.rty = -1;
+    const int cx = g.nx - 1, cy = g.ny - 1, cz = g.nz - 1;
+    const double cell = g.cell;
+    double t_near, t_far;
+    if (!lattice_slab(g, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, t_near, t_far))
+        return false;
     const double t_enter = t_near > 0.0 ? t_near : 0.0;
     const double t_probe = t_enter + 1e-9;
     L.ci = floor_clamp((L.ex + t_probe * L.dx - g.g0[0]) / cell, cx - 1);

@@ -1,0 +1,243 @@
+// lfp_wave.cuh -- wavefront (probe-sorted) traversal of explicit ray
+// batches (sm_100a).
+//
+// Incoherent rays (BASELINE config 5) defeat both one-thread-per-ray
+// schedules: the nested traversal idles most lanes behind the warp's
+// slowest ray, and the persistent state machine (lfp_persistent.cuh) keeps
+// its lanes busy but in different phases (cube set-up, segment set-up,
+// low-res step, high-res step), executed one after another, from a code
+// footprint that misses the instruction cache.
+//
+// Here the unit of work is ONE probe trace of the reference's fall-through
+// (K:603-647). Each iteration, every live ray traces the next probe of its
+// current cube's order (K:758-785) over [max(t_cur, 0), t_exit_cube]; a HIT
+// finishes the ray, a MISS / UNKNOWN moves on (the next corner, or the next
+// cube of the walk, K:801-821) and the ray re-enters the queue keyed by
+// (next probe, where its chord starts and ends on the probe's maps)
+// (wave_key). The queue
+// is radix-sorted by that key between iterations, so the 32 lanes of a
+// warp trace the SAME probe map along nearly the same chord: one code path
+// (probe range -> segments -> low-/high-res DDA), similar step counts,
+// shared texels in L1. Per-ray decisions are the shared
+// helpers of lfp_trace.cuh, so outputs are identical to the other schedules
+// and to the reference; only the order of work changes.
+//
+// Ray state between iterations (indexed by input ray id, 64 B):
+//   double4 (t_max_i, t_max_j, t_max_k, t_cur)             K:715-738
+//   int4    (ci | cj << 10 | ck << 20, corner order, oi | fetches << 4,
+//            best_p)                                       K:758-799
+//   int4    (best texel tx | ty << 16, -, -, -)            K:795-799, 822
+// t_far and the cube steps are recomputed from the ray each iteration with
+// the reference's own ops (bit-identical).
+#pragma once
+
+#include "lfp_persistent.cuh"
+
+namespace lfp {
+
+struct WaveState {
+    double4* tm;
+    int4* cw;
+    int4* bt;
+};
+
+struct WaveRays {
+    const void* ro;      // origins [n][3] (nullptr: shared eye)
+    const void* rd;      // directions [n][3]
+    double3 eye;
+    int f32;
+};
+
+__device__ __forceinline__ void wave_load_ray(const WaveRays& rays, long long i,
+                                              Lane& L)
+{
+    if (rays.f32) {
+        const float* d = (const float*)rays.rd;
+        L.dx = d[3 * i]; L.dy = d[3 * i + 1]; L.dz = d[3 * i + 2];
+        if (rays.ro) {
+            const float* o = (const float*)rays.ro;
+            L.ex = o[3 * i]; L.ey = o[3 * i + 1]; L.ez = o[3 * i + 2];
+        }
+    } else {
+        const double* d = (const double*)rays.rd;
+        L.dx = d[3 * i]; L.dy = d[3 * i + 1]; L.dz = d[3 * i + 2];
+        if (rays.ro) {
+            const double* o = (const double*)rays.ro;
+            L.ex = o[3 * i]; L.ey = o[3 * i + 1]; L.ez = o[3 * i + 2];
+        }
+    }
+    if (!rays.ro) { L.ex = rays.eye.x; L.ey = rays.eye.y; L.ez = rays.eye.z; }
+}
+
+// Sort key of a re-queued ray (scheduling only, never a result): the next
+// probe p, then a 4-D Morton code of the octahedral cells (2^cbits per axis)
+// of the directions from p's origin to the two ends of the ray's range in
+// the current cube -- i.e. where the probe-space chord starts and ends on
+// p's maps. Rays with nearby keys walk nearly the same texels, so a warp's
+// lanes take similar numbers of steps over shared (L1-resident) texels.
+__device__ __forceinline__ void wave_oct_cell(float x, float y, float z,
+                                              float scale, int hi, int& cu,
+                                              int& cv)
+{
+    const float l1 = fabsf(x) + fabsf(y) + fabsf(z);
+    float px = __fdividef(x, l1), pz = __fdividef(z, l1);
+    if (y < 0.0f) {
+        const float fx = (px >= 0.0f ? 1.0f : -1.0f) * (1.0f - fabsf(pz));
+        const float fz = (pz >= 0.0f ? 1.0f : -1.0f) * (1.0f - fabsf(px));
+        px = fx;
+        pz = fz;
+    }
+    int u = (int)floorf((px * 0.5f + 0.5f) * scale);
+    int v = (int)floorf((pz * 0.5f + 0.5f) * scale);
+    cu = u < 0 ? 0 : (u > hi ? hi : u);   // NaN (l1 == 0) -> 0
+    cv = v < 0 ? 0 : (v > hi ? hi : v);
+}
+
+__device__ __forceinline__ unsigned wave_key(const Lane& L, const DevProbes& ps,
+                                             int p, int cbits)
+{
+    const float ox = (float)__ldg(ps.origins + 3 * p + 0);
+    const float oy = (float)__ldg(ps.origins + 3 * p + 1);
+    const float oz = (float)__ldg(ps.origins + 3 * p + 2);
+    const float ex = (float)L.ex - ox, ey = (float)L.ey - oy, ez = (float)L.ez - oz;
+    const float dx = (float)L.dx, dy = (float)L.dy, dz = (float)L.dz;
+    const float t0 = (float)L.t0, t1 = (float)L.t1;
+    const float scale = (float)(1 << cbits);
+    const int hi = (1 << cbits) - 1;
+    int c[4];
+    wave_oct_cell(ex + t0 * dx, ey + t0 * dy, ez + t0 * dz, scale, hi, c[0], c[1]);
+    wave_oct_cell(ex + t1 * dx, ey + t1 * dy, ez + t1 * dz, scale, hi, c[2], c[3]);
+    unsigned m = 0;
+    for (int b = cbits - 1; b >= 0; b--)
+#pragma unroll
+        for (int k = 0; k < 4; k++) m = (m << 1) | ((unsigned)(c[k] >> b) & 1u);
+    return ((unsigned)p << (4 * cbits)) | m;
+}
+
+__device__ __forceinline__ int wave_probe(const Lane& L, const GridParams& g)
+{
+    const int c = (L.order >> (4 * L.oi)) & 15;
+    return L.base + ((c >> 2) & 1) * g.ny * g.nz + ((c >> 1) & 1) * g.nz + (c & 1);
+}
+
+// One iteration for the rays q_in[0..n_in) (q_in == nullptr: identity).
+// `first`: the rays enter the lattice (K:653-713) and are queued for their
+// first probe without tracing it (so that trace is sorted too). Live rays are
+// appended to (key_out, q_out) at positions taken from *n_out; finished
+// rays write their outputs (emit_fn) at their input index.
+template <int MODE, int CFS, typename EmitFn>
+__device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams& g,
+                                          const WaveRays& rays, const WaveState& S,
+                                          const int* __restrict__ q_in,
+                                          long long n_in, int first,
+                                          unsigned* __restrict__ key_out,
+                                          int* __restrict__ q_out,
+                                          unsigned long long* __restrict__ n_out,
+                                          int cbits, ChordF* cfs, EmitFn emit_fn)
+{
+    const unsigned FULL = 0xffffffffu;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < n_in;
+    Diag dg = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, cfs};
+    Lane L;
+    int ray = 0;
+    bool done = false, live = false;
+    unsigned key = 0;
+    if (valid) {
+        ray = q_in ? __ldg(q_in + i) : (int)i;
+        wave_load_ray(rays, ray, L);
+        L.steps = (L.dx > 0.0 ? 1 : 0) | (L.dy > 0.0 ? 2 : 0) | (L.dz > 0.0 ? 4 : 0);
+        bool inside = true;
+        if (first) {
+            inside = lane_ray_init(L, g);
+            if (inside) lane_cube(L, ps, g);
+        } else {
+            double t_near;
+            lattice_slab(g, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, t_near, L.t_far);
+            const double4 tm = S.tm[ray];
+            const int4 cw = S.cw[ray];
+            const int4 bt = S.bt[ray];
+            L.t_max_i = tm.x; L.t_max_j = tm.y; L.t_max_k = tm.z; L.t_cur = tm.w;
+            L.ci = cw.x & 1023; L.cj = (cw.x >> 10) & 1023; L.ck = (cw.x >> 20) & 1023;
+            L.order = (unsigned)cw.y;
+            L.oi = cw.z & 15;
+            L.fetches = (int)((unsigned)cw.z >> 4);
+            L.best_p = cw.w;
+            L.best_tx = bt.x < 0 ? -1 : (bt.x & 0xFFFF);
+            L.best_ty = bt.x < 0 ? -1 : (bt.x >> 16);
+            // K:715-738 increments and K:749-756 cube range (same ops)
+            const double cell = g.cell;
+            L.t_d_i = L.dx != 0.0 ? fabs(cell / L.dx) : CUDART_INF;
+            L.t_d_j = L.dy != 0.0 ? fabs(cell / L.dy) : CUDART_INF;
+            L.t_d_k = L.dz != 0.0 ? fabs(cell / L.dz) : CUDART_INF;
+            L.base = (L.ci * g.ny + L.cj) * g.nz + L.ck;
+            double t_exit_cube = L.t_max_i;
+            if (L.t_max_j < t_exit_cube) t_exit_cube = L.t_max_j;
+            if (L.t_max_k < t_exit_cube) t_exit_cube = L.t_max_k;
+            if (t_exit_cube > L.t_far) t_exit_cube = L.t_far;
+            L.t0 = (0.0 > L.t_cur) ? 0.0 : L.t_cur;
+            L.t1 = t_exit_cube;
+        }
+        bool requeue = false;
+        if (!inside) {
+            done = true;   // misses the lattice: MISS, 0 fetches
+        } else if (first) {
+            requeue = true;   // entered the lattice: sort before tracing
+        } else {
+            // K:603-647: the next probe of the cube's fall-through
+            L.p = wave_probe(L, g);
+            const SegResult s = trace_one_probe<MODE, CFS>(
+                ps, L.p, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, L.t0, L.t1,
+                g.eps_start, g.eps_align, g.slack, dg);
+            L.fetches += s.fetches;
+            if (s.status == HIT) {
+                L.status = HIT; L.rp = L.p; L.rtx = s.tx; L.rty = s.ty;
+                done = true;
+            } else {
+                // the latest UNKNOWN is the walk's diagnostic (K:795-799, 822)
+                if (s.status == UNKNOWN) {
+                    L.best_p = L.p; L.best_tx = s.tx; L.best_ty = s.ty;
+                }
+                L.oi++;
+                if (L.oi == 8) {
+                    if (lane_next_cube(L, g)) {
+                        lane_cube(L, ps, g);
+                    } else {
+                        L.status = MISS; L.rp = L.best_p; L.rtx = L.best_tx;
+                        L.rty = L.best_ty;
+                        done = true;
+                    }
+                }
+                requeue = !done;
+            }
+        }
+        if (requeue) {
+            live = true;
+            key = wave_key(L, ps, wave_probe(L, g), cbits);
+            S.tm[ray] = make_double4(L.t_max_i, L.t_max_j, L.t_max_k, L.t_cur);
+            S.cw[ray] = make_int4(L.ci | (L.cj << 10) | (L.ck << 20),
+                                  (int)L.order,
+                                  (int)(((unsigned)L.fetches << 4) | (unsigned)L.oi),
+                                  L.best_p);
+            S.bt[ray] = make_int4(L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)),
+                                  0, 0, 0);
+        }
+    }
+    // queue the live rays (warp-aggregated slot allocation)
+    const unsigned m = __ballot_sync(FULL, live);
+    if (m) {
+        const int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        const int leader = __ffs(m) - 1;
+        if (lane == leader) base = atomicAdd(n_out, (unsigned long long)__popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (live) {
+            const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+            key_out[pos] = key;
+            q_out[pos] = ray;
+        }
+    }
+    emit_fn(valid && done, ray, L, dg);
+}
+
+}  // namespace lfp

@@ -138,7 +138,7 @@ class DeviceProbeSet:
 
 
 TRACE_MODES = {"filtered": 0, "exact": 1, "check": 2}
-SCHEDULES = {"default": 0, "nested": 1, "persistent": 2}
+SCHEDULES = {"default": 0, "nested": 1, "persistent": 2, "wave": 3}
 
 
 def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG,
@@ -294,6 +294,17 @@ def trace_rays(dps, gparams, origins, dirs, out, rgb_mode=1, stream=None):
         dps.handle, ctypes.byref(gparams), _ptr(origins), _ptr(dirs),
         int(dirs.dtype == torch.float32), dirs.shape[0], ctypes.byref(o),
         ctypes.c_void_p(st.cuda_stream)))
+
+
+# explicit batches of at least this many rays take the wavefront schedule
+# by default (LFP_WAVE_MIN_RAYS in lfp_capi.cu); it sorts rays itself, so
+# binning them first only matters below this size
+WAVE_MIN_RAYS = 1 << 20
+
+
+def last_launches():
+    """Kernels launched by this thread's last explicit-ray trace call."""
+    return int(native.lib().lfp_last_launches())
 
 
 def bin_rays(gparams, origins, dirs, stream=None):

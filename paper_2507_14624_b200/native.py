@@ -85,6 +85,7 @@ def lib():
                              ctypes.c_uint32)
         L.lfp_version.restype = ctypes.c_int
         L.lfp_last_error.restype = ctypes.c_char_p
+        L.lfp_last_launches.restype = ctypes.c_int64
         L.lfp_probeset_create.argtypes = [
             ctypes.c_int, vp, vp, vp, vp, vp, i64, i32, i32, u32, vp,
             ctypes.POINTER(vp)]
@@ -151,4 +152,4 @@ def exported_symbols():
             "lfp_untile", "lfp_bake_probes", "lfp_render_probes",
             "lfp_bin_rays", "lfp_trace_rays_ordered",
             "lfp_probeset_create_packed", "lfp_render_hierarchy",
-            "lfp_bake_points"]
+            "lfp_bake_points", "lfp_last_launches"]

@@ -589,6 +589,33 @@ class TestPersistentSchedule:
         self._same(a, c)
         assert int(c["diag"][4]) == 0
 
+    def test_pcgrid_incoherent_wave(self, golden):
+        """Wavefront schedule: golden reference outputs, shared-eye
+        render_grid path included."""
+        z = golden("pcgrid")
+        grid = golden_grid(z)
+        a = self._run(grid, z["inc_origins"], z["inc_dirs"], "nested")
+        b = self._run(grid, z["inc_origins"], z["inc_dirs"], "wave")
+        c = self._run(grid, z["inc_origins"], z["inc_dirs"], "wave",
+                      ordered=True)
+        self._same(a, b)
+        self._same(a, c)
+        np.testing.assert_array_equal(b["status"], z["inc_status"])
+        np.testing.assert_array_equal(b["fetch"], z["inc_fetch"])
+
+    def test_c5_wave_and_check(self):
+        from paper_2507_14624_b200 import configs
+        scene, grid = configs.c3_grid()
+        o32, d32 = configs.c5_rays(scene, 1 << 17, seed=526)
+        a = self._run(grid, o32, d32, "nested")
+        b = self._run(grid, o32, d32, "wave", ordered=True)
+        c = self._run(grid, o32, d32, "wave", mode="check")
+        e = self._run(grid, o32, d32, "wave", mode="exact")
+        self._same(a, b)
+        self._same(a, c)
+        self._same(a, e)
+        assert int(c["diag"][4]) == 0
+
     def test_camera_persistent(self):
         from paper_2507_14624_b200 import configs
         from paper_2507_14624_b200 import device as dev

@@ -25,7 +25,8 @@ if cfg_name in ("c2", "c3"):
     n = cam.width * cam.height
 else:
     scene, grid = configs.c3_grid()
-    o, d = configs.c5_rays(scene, 1 << 20, seed=505)
+    o, d = configs.c5_rays(scene, 1 << int(os.environ.get("LFP_C5_LOG2", "20")),
+                           seed=505)
     to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
     n = len(o)
 dps = device_probe_set(grid)
