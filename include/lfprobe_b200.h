@@ -182,6 +182,24 @@ int lfp_render_cameras(const lfp_probeset* ps, const lfp_grid_params* grid,
                        int64_t tile_step, int64_t n_tiles, int32_t compact,
                        const lfp_outputs* out, void* stream);
 
+/* render_frame(ProbeGrid, Camera) end to end for one camera: ray
+ * generation, trace and shade as lfp_render_cameras, plus the copy of the
+ * frame into caller HOST buffers (page-locked memory recommended). The
+ * frame is traced in row bands on two internal streams and each band is
+ * copied while later bands trace, so only the last band's copy is exposed.
+ * Blocks until the frame is on the host. host_status (u8 H*W), host_rgb
+ * (f32 H*W*3: HIT radiance, MISS background, UNKNOWN unknown_color) and
+ * host_rgb8 (u8 H*W*3, Frame.rgb8) may each be NULL; stats_out (u64[4]) =
+ * fetch sum, MISS, UNKNOWN, HIT counts; trace_ms_out = device time from the
+ * first band's start to the last band's end. Work is ordered after what is
+ * queued on `stream`, and later work on `stream` after this frame. */
+int lfp_render_frame_host(const lfp_probeset* ps, const lfp_grid_params* grid,
+                          const lfp_camera* cam, int32_t width, int32_t height,
+                          const float* background, const float* unknown_color,
+                          uint8_t* host_status, float* host_rgb,
+                          uint8_t* host_rgb8, uint64_t* stats_out,
+                          float* trace_ms_out, void* stream);
+
 /* render_frame for the non-grid sources (render.py:118-144), same camera
  * batching, frame-ordered outputs:
  *  LFP_SOURCE_SINGLE  one probe, full marching over the padded bounds

@@ -8,6 +8,7 @@ library or GPU raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 import weakref
 
 import numpy as np
@@ -159,7 +160,20 @@ def grid_params(grid_origin, cell, dims, config=DEFAULT_CONFIG,
 
 def camera_struct(cam):
     """Host-side camera parameters computed with the same numpy calls as
-    Camera.basis / Camera.ray_directions (render.py:33-55)."""
+    Camera.basis / Camera.ray_directions (render.py:33-55); memoised per
+    camera value (cameras are immutable)."""
+    params = getattr(type(cam), "__dataclass_params__", None)
+    if params is not None and params.frozen:
+        return _camera_struct_cached(cam)
+    return _camera_struct(cam)
+
+
+@functools.lru_cache(maxsize=4096)
+def _camera_struct_cached(cam):
+    return _camera_struct(cam)
+
+
+def _camera_struct(cam):
     r, u, f = cam.basis()
     tan_v = np.tan(np.radians(cam.vfov_deg) / 2.0)
     tan_h = tan_v * cam.width / cam.height
@@ -232,6 +246,35 @@ def render_cameras(dps, gparams, cams, width, height, out, tile_begin=0,
         tile_begin, tile_step, n_tiles, int(compact), ctypes.byref(o),
         ctypes.c_void_p(st.cuda_stream)))
     return n_tiles
+
+
+def _pinned(shape, dtype):
+    """Page-locked host array from torch's caching host allocator."""
+    return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+
+
+def render_frame_host(dps, gparams, cam, want_rgb=True, want_rgb8=False,
+                      background=(0.0, 0.0, 0.0), unknown_color=(1.0, 0.0, 1.0),
+                      stream=None):
+    """lfp_render_frame_host: one camera end to end into page-locked host
+    arrays -> (status (H, W) u8, rgb (H, W, 3) f32 | None, rgb8 | None,
+    stats u64[4], trace_ms)."""
+    W, H = cam.width, cam.height
+    status = _pinned((H, W), torch.uint8)
+    rgb = _pinned((H, W, 3), torch.float32) if want_rgb else None
+    rgb8 = _pinned((H, W, 3), torch.uint8) if want_rgb8 else None
+    stats = _pinned((4,), torch.int64)
+    bg = (ctypes.c_float * 3)(*[float(v) for v in background])
+    uk = (ctypes.c_float * 3)(*[float(v) for v in unknown_color])
+    ms = ctypes.c_float(0.0)
+    st = stream if stream is not None else torch.cuda.current_stream(dps.device)
+    c = camera_struct(cam)
+    arr = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else None  # noqa: E731
+    native.check(native.lib().lfp_render_frame_host(
+        dps.handle, ctypes.byref(gparams), ctypes.byref(c), W, H, bg, uk,
+        arr(status), arr(rgb), arr(rgb8), arr(stats), ctypes.byref(ms),
+        ctypes.c_void_p(st.cuda_stream)))
+    return status, rgb, rgb8, stats, float(ms.value)
 
 
 def render_probes(dps, kind, cams, width, height, out, gparams, order=None,

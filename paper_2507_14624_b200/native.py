@@ -99,6 +99,10 @@ def lib():
         L.lfp_render_cameras.argtypes = [
             vp, ctypes.POINTER(GridParams), ctypes.POINTER(CameraC), i32, i32,
             i32, i64, i64, i64, i32, ctypes.POINTER(Outputs), vp]
+        L.lfp_render_frame_host.argtypes = [
+            vp, ctypes.POINTER(GridParams), ctypes.POINTER(CameraC), i32, i32,
+            ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), vp,
+            vp, vp, vp, ctypes.POINTER(ctypes.c_float), vp]
         L.lfp_render_probes.argtypes = [
             vp, i32, ctypes.POINTER(i32), i32, ctypes.POINTER(ctypes.c_double),
             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(GridParams),
@@ -128,6 +132,7 @@ def lib():
             ctypes.c_int, vp, vp, i64, vp, i64, i32, i32, u32, vp, vp, vp, vp,
             vp, vp]
         for name in ("lfp_bake_points", "lfp_render_hierarchy", "lfp_probeset_create_packed",
+                     "lfp_render_frame_host",
                      "lfp_bin_rays", "lfp_trace_rays_ordered",
                      "lfp_bake_probes", "lfp_render_probes",
                      "lfp_probeset_create", "lfp_probeset_destroy",
@@ -152,4 +157,4 @@ def exported_symbols():
             "lfp_untile", "lfp_bake_probes", "lfp_render_probes",
             "lfp_bin_rays", "lfp_trace_rays_ordered",
             "lfp_probeset_create_packed", "lfp_render_hierarchy",
-            "lfp_bake_points", "lfp_last_launches"]
+            "lfp_bake_points", "lfp_last_launches", "lfp_render_frame_host"]
