@@ -482,13 +482,22 @@ def e2e_measure(wl, steps, world, rank, local):
         rays, h2d = n, o_h.nbytes + d_h.nbytes
         api = "trace_rays(ProbeGrid, origins, dirs) host f32 arrays -> host results"
     else:
-        cam = wl.cams[rank % len(wl.cams)]
-        n = cam.width * cam.height
+        # this rank's views of one step: one view per GPU (weak-scaled
+        # configs) or its share of the batch (C3: views rank, rank + N, ...)
+        if wl.frames_per_step > 1:
+            cams = wl.cams[rank::world]
+        else:
+            cams = [wl.cams[rank % len(wl.cams)]]
         src = getattr(wl.cfg, "hierarchy", None) or wl.cfg.grid
-        call = lambda: pkg.render_frame(src, cam, device=local)  # noqa: E731
+
+        def call():
+            for cam in cams:
+                pkg.render_frame(src, cam, device=local)
         call()
-        rays, h2d, d2h = n, 104, 13 * n + 32
-        api = "render_frame(ProbeGrid, Camera) -> Frame (host arrays)"
+        n = sum(c.width * c.height for c in cams)
+        rays, h2d, d2h = n, 104 * len(cams), 13 * n + 32 * len(cams)
+        api = ("render_frame(ProbeGrid, Camera) -> Frame (host arrays), "
+               f"{len(cams)} view(s) per step")
     call()
     k = max(3, min(steps, 20))
     if world > 1:
@@ -502,7 +511,9 @@ def e2e_measure(wl, steps, world, rank, local):
     if world > 1 and wl.gather_backend == "nccl":
         tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
     dt = float(te.item())
-    return {"value": world * k * rays / dt / 1e6, "unit": UNIT,
+    total = k * (wl.rays_per_step if wl.frames_per_step > 1 or wl.name == "c5"
+                 else world * rays)
+    return {"value": total / dt / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": api, "call_ms": dt / k * 1e3}
 
