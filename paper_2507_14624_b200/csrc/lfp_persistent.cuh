@@ -269,7 +269,7 @@ __device__ __forceinline__ int lane_transition(Lane& L, int state,
                 int ty = (int)(v * (double)R);
                 if (tx > R - 1) tx = R - 1;
                 if (ty > R - 1) ty = R - 1;
-                const float st = __ldg(ps.dist_hi + ((long long)L.p * R + ty) * R + tx);
+                const float st = __ldg(ps.dist_hi + (long long)L.p * R * R + tex_index(tx, ty, R, ps.ts_hi));
                 L.fetches += 1;
                 if (isfinite(st) && (double)st <= L.t1 * (1.0 + g.slack)) {
                     L.status = HIT; L.rp = L.p; L.rtx = tx; L.rty = ty;
@@ -295,7 +295,7 @@ __device__ __forceinline__ int lane_transition(Lane& L, int state,
                 continue;
             }
             L.c = chord_setup(L.wx, L.wy, L.wz, L.dx, L.dy, L.dz, a, b);
-            dg.segs++;
+            LFP_DIAG(dg.segs++);
             if (MODE >= 1) *L.cf = chord_f(L.c, L.wx, L.wy, L.wz, L.dx, L.dy, L.dz, g.slack);
             else L.cf->ok = false;
             L.margin = chord_margin(L.c, R);
@@ -346,7 +346,7 @@ __device__ __forceinline__ int lane_lo_step(Lane& L, const DevProbes& ps,
     const int res = ps.r;
     L.fetches += lo_fetches(L.lo.ix, L.lo.iy, res);
     const float m_f = __ldg(ps.dil_lo + (long long)L.p * res * res +
-                            L.lo.iy * res + L.lo.ix);
+                            tex_index(L.lo.ix, L.lo.iy, res, ps.ts_lo));
     if (isfinite(m_f)) {
         double s_out = L.lo.t_max_x < L.lo.t_max_y ? L.lo.t_max_x : L.lo.t_max_y;
         if (s_out > 1.0) s_out = 1.0;
@@ -371,7 +371,7 @@ __device__ __forceinline__ int lane_hi_step(Lane& L, const DevProbes& ps,
     const int res = ps.R;
     const long long pbase = (long long)L.p * res * res;
     const int ti = L.hi.iy * res + L.hi.ix;
-    const float stored_f = __ldg(ps.dist_hi + pbase + ti);
+    const float stored_f = __ldg(ps.dist_hi + pbase + tex_index(L.hi.ix, L.hi.iy, res, ps.ts_hi));
     L.fetches += 1;
     if (isfinite(stored_f)) {
         double s_hi = L.hi.t_max_x < L.hi.t_max_y ? L.hi.t_max_x : L.hi.t_max_y;
