@@ -120,6 +120,31 @@ __device__ __forceinline__ int wave_probe(const Lane& L, const GridParams& g)
     return L.base + ((c >> 2) & 1) * g.ny * g.nz + ((c >> 1) & 1) * g.nz + (c & 1);
 }
 
+#ifndef LFP_WAVE_RELOAD
+#define LFP_WAVE_RELOAD 1
+#endif
+
+// The walk state of a re-queued ray (K:715-738 increments recomputed with
+// the reference's ops, bit-identical).
+__device__ __forceinline__ void wave_restore(Lane& L, const GridParams& g,
+                                             const double4 tm, const int4 cw,
+                                             const int4 bt)
+{
+    L.t_max_i = tm.x; L.t_max_j = tm.y; L.t_max_k = tm.z; L.t_cur = tm.w;
+    L.ci = cw.x & 1023; L.cj = (cw.x >> 10) & 1023; L.ck = (cw.x >> 20) & 1023;
+    L.order = (unsigned)cw.y;
+    L.oi = cw.z & 15;
+    L.fetches = (int)((unsigned)cw.z >> 4);
+    L.best_p = cw.w;
+    L.best_tx = bt.x < 0 ? -1 : (bt.x & 0xFFFF);
+    L.best_ty = bt.x < 0 ? -1 : (bt.x >> 16);
+    const double cell = g.cell;
+    L.t_d_i = L.dx != 0.0 ? fabs(cell / L.dx) : CUDART_INF;
+    L.t_d_j = L.dy != 0.0 ? fabs(cell / L.dy) : CUDART_INF;
+    L.t_d_k = L.dz != 0.0 ? fabs(cell / L.dz) : CUDART_INF;
+    L.base = (L.ci * g.ny + L.cj) * g.nz + L.ck;
+}
+
 // One iteration for the rays q_in[0..n_in) (q_in == nullptr: identity).
 // `first`: the rays enter the lattice (K:653-713) and are queued for their
 // first probe without tracing it (so that trace is sorted too). Live rays are
@@ -152,31 +177,27 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
             inside = lane_ray_init(L, g);
             if (inside) lane_cube(L, ps, g);
         } else {
+            // Only what the probe trace needs is computed here (K:749-756,
+            // K:603-605); the rest of the walk state is re-read after the
+            // trace (LFP_WAVE_RELOAD) so it is not live -- spilled to local
+            // memory -- across the trace's loops.
             double t_near;
             lattice_slab(g, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, t_near, L.t_far);
             const double4 tm = S.tm[ray];
             const int4 cw = S.cw[ray];
-            const int4 bt = S.bt[ray];
-            L.t_max_i = tm.x; L.t_max_j = tm.y; L.t_max_k = tm.z; L.t_cur = tm.w;
             L.ci = cw.x & 1023; L.cj = (cw.x >> 10) & 1023; L.ck = (cw.x >> 20) & 1023;
             L.order = (unsigned)cw.y;
             L.oi = cw.z & 15;
-            L.fetches = (int)((unsigned)cw.z >> 4);
-            L.best_p = cw.w;
-            L.best_tx = bt.x < 0 ? -1 : (bt.x & 0xFFFF);
-            L.best_ty = bt.x < 0 ? -1 : (bt.x >> 16);
-            // K:715-738 increments and K:749-756 cube range (same ops)
-            const double cell = g.cell;
-            L.t_d_i = L.dx != 0.0 ? fabs(cell / L.dx) : CUDART_INF;
-            L.t_d_j = L.dy != 0.0 ? fabs(cell / L.dy) : CUDART_INF;
-            L.t_d_k = L.dz != 0.0 ? fabs(cell / L.dz) : CUDART_INF;
             L.base = (L.ci * g.ny + L.cj) * g.nz + L.ck;
-            double t_exit_cube = L.t_max_i;
-            if (L.t_max_j < t_exit_cube) t_exit_cube = L.t_max_j;
-            if (L.t_max_k < t_exit_cube) t_exit_cube = L.t_max_k;
+            double t_exit_cube = tm.x;
+            if (tm.y < t_exit_cube) t_exit_cube = tm.y;
+            if (tm.z < t_exit_cube) t_exit_cube = tm.z;
             if (t_exit_cube > L.t_far) t_exit_cube = L.t_far;
-            L.t0 = (0.0 > L.t_cur) ? 0.0 : L.t_cur;
+            L.t0 = (0.0 > tm.w) ? 0.0 : tm.w;
             L.t1 = t_exit_cube;
+#if !LFP_WAVE_RELOAD
+            wave_restore(L, g, tm, cw, S.bt[ray]);
+#endif
         }
         bool requeue = false;
         if (!inside) {
@@ -189,6 +210,19 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
             const SegResult s = trace_one_probe<MODE, CFS>(
                 ps, L.p, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, L.t0, L.t1,
                 g.eps_start, g.eps_align, g.slack, dg);
+#if LFP_WAVE_RELOAD
+            {
+                // opaque copies that depend on the trace's result: the
+                // compiler can neither reuse the loads above nor hoist these
+                // above the trace
+                const double4* tmp = S.tm;
+                const int4* cwp = S.cw;
+                const int4* btp = S.bt;
+                asm volatile("" : "+l"(tmp), "+l"(cwp), "+l"(btp)
+                             : "r"(s.status), "r"(s.fetches));
+                wave_restore(L, g, tmp[ray], cwp[ray], btp[ray]);
+            }
+#endif
             L.fetches += s.fetches;
             if (s.status == HIT) {
                 L.status = HIT; L.rp = L.p; L.rtx = s.tx; L.rty = s.ty;
