@@ -158,12 +158,15 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                                           unsigned* __restrict__ key_out,
                                           int* __restrict__ q_out,
                                           unsigned long long* __restrict__ n_out,
-                                          int cbits, ChordF* cfs, EmitFn emit_fn)
+                                          int cbits, ChordF* cfs, Chord* chs,
+                                          Range* rgs, EmitFn emit_fn)
 {
     const unsigned FULL = 0xffffffffu;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = i < n_in;
     Diag dg = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, cfs};
+    dg.chs = chs;
+    dg.rgs = rgs;
     Lane L;
     int ray = 0;
     bool done = false, live = false;
