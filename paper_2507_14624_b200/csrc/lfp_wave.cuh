@@ -123,6 +123,9 @@ __device__ __forceinline__ int wave_probe(const Lane& L, const GridParams& g)
 #ifndef LFP_WAVE_RELOAD
 #define LFP_WAVE_RELOAD 1
 #endif
+#ifndef LFP_WAVE_RELOAD_RAY
+#define LFP_WAVE_RELOAD_RAY 0
+#endif
 
 // The walk state of a re-queued ray (K:715-738 increments recomputed with
 // the reference's ops, bit-identical).
@@ -224,6 +227,13 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                 asm volatile("" : "+l"(tmp), "+l"(cwp), "+l"(btp)
                              : "r"(s.status), "r"(s.fetches));
                 wave_restore(L, g, tmp[ray], cwp[ray], btp[ray]);
+#if LFP_WAVE_RELOAD_RAY
+                // the ray too: its origin is dead once the trace has formed
+                // w = e - origin, so it is not kept (spilled) across the trace
+                WaveRays rr = rays;
+                asm volatile("" : "+l"(rr.rd), "+l"(rr.ro) : "r"(s.status));
+                wave_load_ray(rr, ray, L);
+#endif
             }
 #endif
             L.fetches += s.fetches;
