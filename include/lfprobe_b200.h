@@ -279,6 +279,15 @@ int lfp_untile(int32_t n_cams, int32_t width, int32_t height, int32_t n_ranks,
                const float* rgb_in, uint8_t* status_out, float* rgb_out,
                void* stream);
 
+/* Diagnostics: ref[i] = a[i] / b[i] (nvcc IEEE division); fast[i] = the
+ * tracer's branch-free division of the same operands (LFP_FAST_DIV: the
+ * fast-path quotient when nvcc's fast-path test passes, else a / b) and
+ * took[i] = 1 when it passed (device arrays). The GPU tests assert fast ==
+ * ref bit for bit. */
+int lfp_selftest_division(const double* a, const double* b, int64_t n,
+                          double* ref, double* fast, uint8_t* took,
+                          void* stream);
+
 /* ---- input production: GPU ray-cast bake ---- */
 
 /* Analytic primitive: kind 0 = axis-aligned box (a = lo, b = hi), kind 1 =

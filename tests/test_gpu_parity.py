@@ -647,3 +647,43 @@ class TestPersistentSchedule:
             res[-1]["compact"] = o2.status.cpu().numpy()
         for k in res[0]:
             np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)
+
+
+@pytest.mark.gpu
+def test_branch_free_division_is_ieee():
+    """The tracer's branch-free division (rcp_nv / div_nv, LFP_FAST_DIV)
+    equals nvcc's IEEE `a / b` bit for bit whenever its fast-path test
+    passes (and falls back to `a / b` otherwise): random operands over the
+    magnitudes the tracer sees, wide exponents, signs, zeros, infinities,
+    NaN, subnormals; the fast path must be the common case."""
+    import ctypes
+    from paper_2507_14624_b200 import native
+    rng = np.random.default_rng(11)
+    n = 1 << 21
+    a = rng.normal(size=n) * 10.0 ** rng.uniform(-6, 6, n)
+    b = rng.normal(size=n) * 10.0 ** rng.uniform(-6, 6, n)
+    a[: n // 4] = rng.uniform(-4, 4, n // 4)
+    b[: n // 4] = rng.uniform(0.01, 3, n // 4)
+    ex = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 5e-324, 1e-310,
+                   1e308, 1.7976931348623157e308, 2.2250738585072014e-308,
+                   3.0, 7.0, 1e-200, 1e200])
+    aa, bb = np.meshgrid(ex, ex)
+    a = np.concatenate([a, aa.ravel(), 2.0 ** rng.integers(-1070, 1023, 4096)])
+    b = np.concatenate([b, bb.ravel(), 2.0 ** rng.integers(-1070, 1023, 4096)
+                        * rng.uniform(1, 2, 4096)])
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    ref = torch.empty_like(ta)
+    fast = torch.empty_like(ta)
+    took = torch.empty(len(a), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    native.check(native.lib().lfp_selftest_division(
+        ctypes.c_void_p(ta.data_ptr()), ctypes.c_void_p(tb.data_ptr()), len(a),
+        ctypes.c_void_p(ref.data_ptr()), ctypes.c_void_p(fast.data_ptr()),
+        ctypes.c_void_p(took.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
+    torch.cuda.synchronize()
+    r, f = ref.cpu().numpy(), fast.cpu().numpy()
+    bad = r.view(np.uint64) != f.view(np.uint64)
+    assert int((bad & ~(np.isnan(r) & np.isnan(f))).sum()) == 0
+    with np.errstate(all="ignore"):
+        np.testing.assert_array_equal(r, a / b)
+    assert took[:n].float().mean().item() > 0.99
