@@ -1,22 +1,31 @@
 """Benchmark: probe-traced Mrays/s (and frames/s) of the B200 grid tracer.
 
-    python bench.py [--gpus N --steps K --warmup W --config c2|c1|c3|c5]
+    python bench.py [--gpus N --steps K --warmup W --config c3|c1|c2|c4|c5]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # CPU reference arm (oracle port)
 
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU); under torchrun the world
+size must equal N.
+
 Workloads (BASELINE.json configs, seeded synthetic inputs, configs.py):
-  c2 (default) 4x4x4 probes 128^2/32^2, one 512x512 view per GPU per step.
+  c3 (default; BASELINE configs[2], the largest single-GPU configuration)
+     8x4x8 probes 256^2/64^2 (fp16 payloads), 64 poses at 1920x1080 per
+     step, 8x16 tiles interleaved over the N ranks (strong scaling), rank 0
+     gathers the framebuffer over NCCL and untiles it.
+  c2 4x4x4 probes 128^2/32^2, one 512x512 view per GPU per step.
      Weak scaling: the global batch has N views; its 8x16 pixel tiles are
      interleaved over the ranks, each rank traces its tiles against its own
      probe-set replica, rank 0 gathers the framebuffer over NCCL (the only
      collective) and untiles it.
   c1 the same with the 2x2x2 / 32^2 room and a 128x128 view.
-  c3 8x4x8 probes 256^2/64^2 (fp16 payloads), 64 poses at 1920x1080 per
-     step, tiles interleaved over the N ranks (strong scaling).
+  c4 3-level 128^2/32^2 hierarchy (9,344 probes), one 3840x2160 view per
+     GPU per step.
   c5 the c3 probe set, 2^26 incoherent f32 rays per step split into N
      contiguous batches (strong scaling); each rank bins its rays by
      (entry cube, direction octant), sorts and traces them in bin order,
-     rank 0 gathers the per-ray results.
+     rank 0 gathers every per-ray output (status, probe, texel, fetch, rgb,
+     hit distance).
 Inputs (probe set, cameras / rays) are resident in HBM before the timed
 region. L2 (126 MB) is flushed between steps by a 512 MiB write outside the
 timed events (the c2 probe set, 28 MB, would otherwise stay L2-resident).
@@ -140,16 +149,18 @@ def gpu_smi_id(torch, dev_index):
         return dev_index
 
 
-def build_config(name, views):
+def build_config(name, views, device=0):
+    """The seeded config; GPU bakes (C3/C5 probe set, C4 hierarchy) run on
+    this rank's own `device` (every rank bakes an identical replica)."""
     from paper_2507_14624_b200 import configs
     if name == "c1":
         return configs.c1()
     if name == "c2":
         return configs.c2(n_views=views)
     if name in ("c3", "c5"):
-        return configs.c3(n_views=views)
+        return configs.c3(n_views=max(views, 1), device=device)
     if name == "c4":
-        return configs.c4(n_views=views)
+        return configs.c4(n_views=views, device=device)
     raise SystemExit(f"unknown config {name}")
 
 
@@ -191,18 +202,47 @@ def config_record(cfg, name, world, views):
 # CPU reference arm / baseline (the oracle port -- test infrastructure)
 # --------------------------------------------------------------------------
 
-def cpu_sample(cfg, name, stride):
-    """Bounded sample of the workload: every `stride`-th ray of view 0 (or
-    of the C5 ray set), f64, directions computed exactly as render.py."""
+# Bounded CPU samples of one step's workload (fraction of its rays):
+#   c1, c2  every ray of the view (same_config holds for the reference arm)
+#   c3      a seeded 1/FRAC subsample of the pixels of all 64 poses
+#   c4      a seeded 1/FRAC subsample of the 4K view
+#   c5      the first 2^26/FRAC rays of the bench ray set
+REF_FRAC = {"c1": 1, "c2": 1, "c3": 64, "c4": 64, "c5": 256}
+CPU_FRAC = {"c1": 1, "c2": 1, "c3": 256, "c4": 256, "c5": 256}
+NUMBA_NOTE = ("the C port runs ~2.2x faster than the numba reference "
+              "itself on the same host (C2, 8 cores: 1.03 vs 0.476 Mrays/s, "
+              "identical outputs), so this baseline is conservative")
+
+
+def cpu_sample(cfg, name, frac, seed=12345):
+    """(origins (N, 3) f64 or eye (3,), dirs (N, 3) f64, description) of a
+    bounded sample of one step's workload; directions computed in the
+    reference's op order (render.py:50-62) by the oracle."""
     from oracle import oracle
     if name == "c5":
         from paper_2507_14624_b200 import configs
-        o, d = configs.c5_rays(cfg.scene, C5_RAYS // stride, seed=505)
-        return o.astype(np.float64), d.astype(np.float64)
-    cam = cfg.cameras[0]
-    basis, tv, th = oracle.camera_params(cam)
-    dirs = oracle.camera_dirs(basis, tv, th, cam.width, cam.height)
-    return np.asarray(cam.eye, np.float64), np.ascontiguousarray(dirs[::stride])
+        o, d = configs.c5_rays(cfg.scene, C5_RAYS // frac)
+        return (o.astype(np.float64), d.astype(np.float64),
+                f"the first {C5_RAYS // frac} rays of the C5 ray set")
+    rng = np.random.default_rng(seed)
+    os_, ds_ = [], []
+    for cam in cfg.cameras:
+        basis, tv, th = oracle.camera_params(cam)
+        dirs = oracle.camera_dirs(basis, tv, th, cam.width, cam.height)
+        if frac > 1:
+            idx = np.sort(rng.choice(len(dirs), len(dirs) // frac,
+                                     replace=False))
+            dirs = dirs[idx]
+        ds_.append(dirs)
+        os_.append(np.broadcast_to(np.asarray(cam.eye, np.float64),
+                                   dirs.shape))
+    what = (f"every ray of {len(cfg.cameras)} view(s)" if frac == 1 else
+            f"a seeded 1/{frac} pixel subsample of all {len(cfg.cameras)} "
+            "view(s)")
+    if len(cfg.cameras) == 1:
+        return np.asarray(cfg.cameras[0].eye, np.float64), ds_[0], what
+    return (np.ascontiguousarray(np.concatenate(os_)),
+            np.ascontiguousarray(np.concatenate(ds_)), what)
 
 
 def run_cpu(cfg, eye, dirs):
@@ -217,18 +257,13 @@ def run_cpu(cfg, eye, dirs):
     return time.perf_counter() - t0, res
 
 
-CPU_STRIDE = {"c1": 1, "c2": 1, "c3": 16, "c4": 64, "c5": 256}
-REF_STRIDE = {"c1": 1, "c2": 4, "c3": 64, "c4": 256, "c5": 512}
-
-
 def cpu_baseline(cfg, name, budget_s=12.0):
     """Oracle port on all host threads over repeated passes of a bounded
     sample, ~budget_s of CPU time."""
     from oracle import oracle
     threads = os.cpu_count() or 1
     oracle.set_num_threads(threads)
-    stride = CPU_STRIDE[name]
-    eye, dirs = cpu_sample(cfg, name, stride)
+    eye, dirs, what = cpu_sample(cfg, name, CPU_FRAC[name])
     run_cpu(cfg, eye if eye.ndim == 1 else eye[:4096], dirs[:4096])  # warm
     total_t, total_n, reps = 0.0, 0, 0
     while total_t < budget_s or reps == 0:
@@ -240,22 +275,22 @@ def cpu_baseline(cfg, name, budget_s=12.0):
             break
     return {"value": total_n / total_t / 1e6, "unit": UNIT, "cores": threads,
             "kind": "port",
-            "sample": f"{reps} pass(es) over every {stride}-th ray of "
-                      f"{'the C5 ray set' if name == 'c5' else 'view 0'} "
-                      f"({len(dirs)} rays/pass), C oracle (oracle/lfp_oracle.c"
-                      f", OpenMP {threads} threads)"}
+            "sample": f"{reps} pass(es) over {what} ({len(dirs)} rays/pass), "
+                      f"C oracle (oracle/lfp_oracle.c, OpenMP {threads} "
+                      "threads)",
+            "note": NUMBA_NOTE}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cfg = build_config(args.config, 1)
+    cfg = build_config(args.config, 64 if args.config == "c3" else 1)
     from oracle import oracle
     threads = os.cpu_count() or 1
     oracle.set_num_threads(threads)
-    stride = REF_STRIDE[args.config]
-    eye, dirs = cpu_sample(cfg, args.config, stride)
+    frac = REF_FRAC[args.config]
+    eye, dirs, what = cpu_sample(cfg, args.config, frac)
     for _ in range(args.warmup):
         run_cpu(cfg, eye, dirs)
     times = []
@@ -265,21 +300,21 @@ def run_reference(args):
         times.append(dt)
     t = sum(times)
     value = len(dirs) * args.steps / t / 1e6
-    what = "the C5 ray set" if args.config == "c5" else "view 0"
+    views = len(cfg.cameras) if args.config != "c5" else 0
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak" if args.config in ("c1", "c2") else "strong",
+        "scaling": "weak" if args.config in ("c1", "c2", "c4") else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded scene, ray-cast bake)",
-        "config": config_record(cfg, args.config, 1, 1) | {
-            "reference_sample": f"every {stride}-th ray of {what} per step "
-                                f"({len(dirs)} rays)"},
+        "config": config_record(cfg, args.config, 1, views) | {
+            "reference_sample": f"{what} per step ({len(dirs)} rays)",
+            "same_config": frac == 1},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
                          "kind": "port",
-                         "sample": f"{len(dirs)} rays per step (every "
-                                   f"{stride}-th ray of {what})"},
+                         "sample": f"{len(dirs)} rays per step ({what})",
+                         "note": NUMBA_NOTE},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "fetch_per_ray": float(res.fetch.mean()),
@@ -304,7 +339,6 @@ class Workload:
         from paper_2507_14624_b200.trace import DEFAULT_CONFIG
         self.torch, self.dev, self.pdist = torch, dev, pdist
         self.name, self.world, self.rank, self.dvc = args.config, world, rank, dvc
-        self.gather_backend = args.dist_backend
         name = args.config
         if name in ("c1", "c2", "c4"):
             self.views = args.views or 1
@@ -313,7 +347,7 @@ class Workload:
             self.views = views_total = args.views or 64   # strong scaling
         else:
             self.views = views_total = 1
-        self.cfg = build_config(name, views_total)
+        self.cfg = build_config(name, views_total, device=dvc.index)
         self.dps = device_probe_set(self.cfg.grid, dvc.index)
         self.levels = None
         if name == "c4":
@@ -333,14 +367,15 @@ class Workload:
         self.binned = False
         if name == "c5":
             from paper_2507_14624_b200 import configs
-            lo = rank * C5_RAYS // world
-            hi = (rank + 1) * C5_RAYS // world
-            o, d = configs.c5_rays(self.cfg.scene, C5_RAYS, seed=505)
-            self.o = torch.from_numpy(o[lo:hi].copy()).to(dvc)
-            self.d = torch.from_numpy(d[lo:hi].copy()).to(dvc)
+            lo, hi = pdist.ray_share(C5_RAYS, world, rank)
+            o, d = configs.c5_rays(self.cfg.scene, hi - lo, start=lo)
+            self.o = torch.from_numpy(o).to(dvc)
+            self.d = torch.from_numpy(d).to(dvc)
             self.n_local = hi - lo
             self.max_local = (C5_RAYS + world - 1) // world
-            self.out = dev.RayOutputs(self.max_local, dvc)
+            # every per-ray output of trace_grid_ray (K:653-657) + hit_t
+            self.out = dev.RayOutputs(self.max_local, dvc, probe=True,
+                                      texel=True, fetch=True, hit_t=True)
             self.out.status.zero_()
             self.out.rgb.zero_()
             self.extra_in_bytes = 24
@@ -375,13 +410,14 @@ class Workload:
         """The traced launch(es) of one step on this rank (no collective)."""
         dev = self.dev
         if self.name == "c5":
+            out = self.out
             if self.binned:
                 keys = dev.bin_rays(self.g, self.o, self.d, stream=self.stream)
                 order = dev.ray_order(keys)
                 dev.trace_rays_ordered(self.dps, self.g, self.o, self.d, order,
-                                       self.out, stream=self.stream)
+                                       out, stream=self.stream)
             else:
-                dev.trace_rays(self.dps, self.g, self.o, self.d, self.out,
+                dev.trace_rays(self.dps, self.g, self.o, self.d, out,
                                stream=self.stream)
             self.launches = dev.last_launches()
             return
@@ -409,15 +445,15 @@ class Workload:
         """Framebuffer (or per-ray result) gather to rank 0 + untile."""
         if self.world == 1:
             return
-        torch, pdist = self.torch, self.pdist
-        st, rgb = self.out.status, self.out.rgb
-        if self.gather_backend == "gloo":
-            st, rgb = st.cpu(), rgb.cpu()
+        pdist = self.pdist
+        o = self.out
         if self.name == "c5":
-            g = gather_padded(st, rgb, self.max_local)
-        else:
-            g = pdist.gather_shards(self.plan, st, rgb)
-        if g is None or self.name == "c5":
+            pdist.gather_rows([o.status, o.probe, o.texel, o.fetch, o.rgb,
+                               o.hit_t], self.max_local)
+            return
+        g = pdist.gather_shards(self.plan, pdist._comm(o.status),
+                                pdist._comm(o.rgb))
+        if g is None:
             return
         st_all, rgb_all = (t.to(self.dvc) for t in g)
         self.dev.untile(len(self.cams), self.W, self.H, self.world, st_all,
@@ -442,92 +478,97 @@ class Workload:
         return (4 * f + 12 * h + (16 + self.extra_in_bytes) * n, n, f, h)
 
 
-def gather_padded(st, rgb, m):
-    """Gather equal-size (padded) per-rank result buffers to rank 0."""
-    import torch
-    import torch.distributed as tdist
-    world = tdist.get_world_size()
-    if st.shape[0] < m:
-        st = torch.nn.functional.pad(st, (0, m - st.shape[0]))
-        rgb = torch.nn.functional.pad(rgb, (0, 0, 0, m - rgb.shape[0]))
-    if tdist.get_rank() == 0:
-        st_l = [torch.empty_like(st) for _ in range(world)]
-        rgb_l = [torch.empty_like(rgb) for _ in range(world)]
-    else:
-        st_l = rgb_l = None
-    tdist.gather(st, st_l, dst=0)
-    tdist.gather(rgb, rgb_l, dst=0)
-    if tdist.get_rank() == 0:
-        return torch.cat(st_l), torch.cat(rgb_l)
-    return None
-
-
 def e2e_measure(wl, steps, world, rank, local):
-    """Same metric through the public API with host buffers: render_frame
-    (camera configs) or trace_rays (C5) -- H2D of the step's inputs and
-    D2H of its results inside the timed region, per rank."""
+    """Same metric through the public API with host buffers, H2D of the
+    step's inputs and D2H of its results inside the timed region:
+      N = 1: render_frame(grid, cam) per camera (the reference's call,
+             render.py:102) / trace_rays(grid, origins, dirs) for C5;
+      N > 1: dist.render_frames(grid, cams) / dist.trace_rays_sharded --
+             per-rank trace, the gather to rank 0, untile and D2H there.
+    Timed with CUDA events on the current stream, max over ranks."""
     import torch
     import torch.distributed as tdist
 
     import paper_2507_14624_b200 as pkg
+    from paper_2507_14624_b200 import dist as pdist
     if wl.name == "c5":
-        n = wl.n_local                       # this rank's whole share
-        o_h = wl.o[:n].cpu().numpy()
-        d_h = wl.d[:n].cpu().numpy()
-        call = lambda: pkg.trace_rays(wl.cfg.grid, o_h, d_h, device=local)  # noqa: E731
-        r = call()
-        d2h = sum(a.nbytes for a in (r.status, r.probe, r.tx, r.ty, r.fetch,
-                                     r.rgb, r.hit_t, r.stats))
-        del r
-        rays, h2d = n, o_h.nbytes + d_h.nbytes
-        api = "trace_rays(ProbeGrid, origins, dirs) host f32 arrays -> host results"
-    else:
-        # this rank's views of one step: one view per GPU (weak-scaled
-        # configs) or its share of the batch (C3: views rank, rank + N, ...)
-        if wl.frames_per_step > 1:
-            cams = wl.cams[rank::world]
+        from paper_2507_14624_b200 import configs
+        if world == 1:
+            o_h = wl.o.cpu().numpy()
+            d_h = wl.d.cpu().numpy()
+            call = lambda: pkg.trace_rays(wl.cfg.grid, o_h, d_h, device=local)  # noqa: E731
+            api = ("trace_rays(ProbeGrid, origins, dirs) host f32 arrays -> "
+                   "host results")
         else:
-            cams = [wl.cams[rank % len(wl.cams)]]
+            o_h, d_h = configs.c5_rays(wl.cfg.scene, C5_RAYS)
+            call = lambda: pdist.trace_rays_sharded(  # noqa: E731
+                wl.cfg.grid, o_h, d_h, device=local)
+            api = ("dist.trace_rays_sharded(ProbeGrid, origins, dirs): host "
+                   "f32 arrays, per-rank share, gather of every per-ray "
+                   "output to rank 0, D2H there")
+        rays = C5_RAYS
+        h2d = o_h.nbytes + d_h.nbytes
+        d2h = rays * (1 + 4 * 4 + 12 + 4) + 32
+    else:
         src = getattr(wl.cfg, "hierarchy", None) or wl.cfg.grid
+        if world == 1:
+            cams = wl.cams
 
-        def call():
-            for cam in cams:
-                pkg.render_frame(src, cam, device=local)
-        call()
-        n = sum(c.width * c.height for c in cams)
-        rays, h2d, d2h = n, 104 * len(cams), 13 * n + 32 * len(cams)
-        api = ("render_frame(ProbeGrid, Camera) -> Frame (host arrays), "
-               f"{len(cams)} view(s) per step")
+            def call():
+                for cam in cams:
+                    pkg.render_frame(src, cam, device=local)
+            api = (f"render_frame(grid, Camera) -> Frame (host arrays), "
+                   f"{len(cams)} call(s) per step")
+        else:
+            cams = wl.cams
+            call = lambda: pdist.render_frames(src, cams, device=local)  # noqa: E731
+            api = (f"dist.render_frames(grid, {len(cams)} cameras) -> Frames "
+                   "on rank 0: tile-sharded trace, NCCL gather, untile, D2H")
+        rays = sum(c.width * c.height for c in cams)
+        h2d, d2h = 104 * len(cams), 13 * rays + 32 * len(cams)
     call()
     k = max(3, min(steps, 20))
+    stream = torch.cuda.current_stream(wl.dvc)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    e0.record(stream)
     for _ in range(k):
         call()
-    dt = time.perf_counter() - t0
-    te = torch.tensor([dt], dtype=torch.float64, device=wl.dvc)
-    if world > 1 and wl.gather_backend == "nccl":
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) * 1e-3
+    te = torch.tensor([dt], dtype=torch.float64)
+    if world > 1:
+        te = pdist._comm(te.to(wl.dvc))
         tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
     dt = float(te.item())
-    total = k * (wl.rays_per_step if wl.frames_per_step > 1 or wl.name == "c5"
-                 else world * rays)
-    return {"value": total / dt / 1e6, "unit": UNIT,
+    return {"value": k * rays / dt / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": api, "call_ms": dt / k * 1e3}
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2",
+    ap.add_argument("--config", default="c3",
                     choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--views", type=int, default=0,
-                    help="views per step (per GPU for c1/c2, total for c3)")
+                    help="views per step (per GPU for c1/c2/c4, total for c3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-binning", action="store_true",
@@ -540,7 +581,7 @@ def main():
     ap.add_argument("--schedule", default="default",
                     choices=["default", "nested", "persistent", "wave"],
                     help="traversal schedule (default: nested for cameras, "
-                         "persistent for explicit rays)")
+                         "wavefront for >= 2^20 explicit rays)")
     ap.add_argument("--min-active", type=int, default=0,
                     help="persistent schedule stepping threshold (0 = 16)")
     ap.add_argument("--lib", default=None,
@@ -556,11 +597,21 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
+
     import torch
     import torch.distributed as tdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dvc = torch.device("cuda", local)
@@ -620,8 +671,7 @@ def main():
         cpu = cpu_baseline(wl.cfg, args.config, args.cpu_budget)
 
     if rank == 0:
-        kernel = {"c5": ("wave_kernel: all wavefront iterations of the step "
-                         "incl. the CUB sorts between them"
+        kernel = {"c5": ("wave_kernel: all wavefront iterations of the step"
                          if wl.launches > 1 else
                          "trace_rays_kernel / persistent_kernel" +
                          (" (binned)" if wl.binned else "")),
@@ -660,7 +710,7 @@ def main():
             "lib": os.path.basename(os.environ.get("LFP_LIB_PATH", "")) or
                    "liblfprobe_b200.so",
         }
-        if args.dist_backend != "nccl":
+        if args.dist_backend != "nccl" and world > 1:
             line["dist_backend"] = args.dist_backend
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -158,16 +158,31 @@ def c4(seed=404, cam_seed=4404, n_views=1, width=3840, height=2160, device=0):
     return cfg
 
 
-def c5_rays(scene, n, seed=505):
-    """Incoherent rays: origins U(interior), directions normalised Gaussian
-    (`pkg/tests/conftest.py:29-31`), both stored as float32."""
-    rng = np.random.default_rng(seed)
+C5_BLOCK = 1 << 20
+
+
+def c5_rays(scene, n, seed=505, start=0):
+    """Incoherent rays [start, start + n) of the seeded C5 ray sequence:
+    origins U(interior), directions normalised Gaussian
+    (`pkg/tests/conftest.py:29-31`), both stored as float32. The sequence
+    is generated in blocks of 2^20 rays, block b from default_rng([seed, b]),
+    so any slice (a rank's share, the first 2^20 rays of the bench set) is
+    reproducible without generating the whole 2^26-ray set."""
     lo = np.asarray(scene.interior_lo, np.float64)
     hi = np.asarray(scene.interior_hi, np.float64)
-    o = rng.uniform(lo, hi, size=(n, 3)).astype(np.float32)
-    d = rng.normal(size=(n, 3))
-    d /= np.linalg.norm(d, axis=-1, keepdims=True)
-    return o, d.astype(np.float32)
+    o = np.empty((n, 3), np.float32)
+    d = np.empty((n, 3), np.float32)
+    b0, b1 = start // C5_BLOCK, (start + n + C5_BLOCK - 1) // C5_BLOCK
+    for b in range(b0, b1):
+        rng = np.random.default_rng([seed, b])
+        bo = rng.uniform(lo, hi, size=(C5_BLOCK, 3)).astype(np.float32)
+        bd = rng.normal(size=(C5_BLOCK, 3))
+        bd /= np.linalg.norm(bd, axis=-1, keepdims=True)
+        s0 = max(start, b * C5_BLOCK)
+        s1 = min(start + n, (b + 1) * C5_BLOCK)
+        o[s0 - start:s1 - start] = bo[s0 - b * C5_BLOCK:s1 - b * C5_BLOCK]
+        d[s0 - start:s1 - start] = bd[s0 - b * C5_BLOCK:s1 - b * C5_BLOCK]
+    return o, d
 
 
 def probe_set_digest(ps):

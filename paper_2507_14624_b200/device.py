@@ -400,14 +400,38 @@ def untile(n_cams, width, height, n_ranks, status_in, rgb_in, status_out,
 
 
 # ---- probe-set cache: one device copy per (host arrays, device) ----------
+#
+# Contract (as the reference's, grid.py:76-80, which stacks a grid's arrays
+# once and reuses them): probe arrays handed to the tracer are immutable.
+# The cache is keyed on the arrays' identity, so an in-place edit of a
+# cached array is NOT seen by later calls unless
+#   * `invalidate(array)` is called after the edit, or
+#   * content verification is on (`VERIFY_CONTENT = True`, or the
+#     environment variable LFP_VERIFY_PROBE_CONTENT=1): every lookup then
+#     re-hashes the arrays (blake2b over their bytes, ~1 GB/s on the host)
+#     and re-uploads on a change -- the numba kernel's semantics of reading
+#     the arrays on every call (kernels.py:825-843), at host-hash cost.
+
+import hashlib
+import os
 
 _CACHE = {}
+VERIFY_CONTENT = os.environ.get("LFP_VERIFY_PROBE_CONTENT", "0") == "1"
+
+
+def _fingerprint(arrs):
+    h = hashlib.blake2b(digest_size=16)
+    for a in arrs:
+        a = np.ascontiguousarray(a)
+        h.update(str((a.dtype.str, a.shape)).encode())
+        h.update(memoryview(a).cast("B"))
+    return h.digest()
 
 
 def cached_probe_set(dist_hi, dir_hi, irr_hi, dist_lo, origins, device=0):
     """Device probe set for these exact host arrays (identity-keyed, like
     the reference's cached ProbeSet, grid.py:76-80). The arrays are treated
-    as immutable, as the reference does."""
+    as immutable, as the reference does; see the contract above."""
     arrs = (dist_hi, dir_hi, irr_hi, dist_lo, origins)
     return cached_for(arrs, lambda: arrs, device)
 
@@ -417,22 +441,37 @@ def register(dps, key_objs, device=0):
     return cached_for(key_objs, None, device, dps=dps)
 
 
+def invalidate(*objs):
+    """Drop every cached device probe set built from any of `objs` (call
+    after editing a probe array in place)."""
+    ids = {id(o) for o in objs}
+    for key in [k for k in _CACHE if ids & set(k[:-1])]:
+        _CACHE.pop(key, None)
+
+
 def cached_for(key_objs, arrays_fn, device=0, dps=None):
     """Device probe set cached on the identity of `key_objs` (weakly held);
     `arrays_fn()` yields the five host arrays on a miss."""
     key = tuple(id(a) for a in key_objs) + (int(device),)
     hit = _CACHE.get(key) if dps is None else None
+    fp = None
     if hit is not None:
-        refs, cached = hit
+        refs, cached, cached_fp = hit
         if all(r() is a for r, a in zip(refs, key_objs)):
-            return cached
+            if not VERIFY_CONTENT:
+                return cached
+            fp = _fingerprint(key_objs)
+            if fp == cached_fp:
+                return cached
     if dps is None:
         dps = DeviceProbeSet(*arrays_fn(), device=device)
     try:
         refs = tuple(weakref.ref(a) for a in key_objs)
     except TypeError:
         return dps
-    _CACHE[key] = (refs, dps)
+    if fp is None and VERIFY_CONTENT:
+        fp = _fingerprint(key_objs)
+    _CACHE[key] = (refs, dps, fp)
     for r in refs:   # drop the entry when any key object dies
         weakref.finalize(r(), _CACHE.pop, key, None)
     return dps

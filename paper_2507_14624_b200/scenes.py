@@ -307,3 +307,27 @@ def sample_point_cloud(scene, density, seed=0):
             pts.append(np.asarray(prim.center) + prim.radius * v)
             cols.append(np.broadcast_to(prim.albedo, (n, 3)))
     return PointCloud(np.concatenate(pts), np.concatenate(cols).astype(np.float32))
+
+
+# The reference's fixed test room (`scenes.py:249-270`: a 3 m x 2.5 m x 6 m
+# room, x width, y height, z length, with two interior boxes), used by the
+# acceptance-style GPU tests (`pkg/tests/test_acceptance.py`) together with
+# sample_point_cloud and the point-cloud bake. Geometry only; one albedo per
+# primitive (the reference's per-face wall colours do not affect tracing).
+ACCEPTANCE_ROOM = (3.0, 2.5, 6.0)
+
+
+def acceptance_room(with_boxes=True, extra=()):
+    w, h, l = ACCEPTANCE_ROOM
+    prims = [Box((0.0, 0.0, 0.0), (w, h, l), albedo=(0.5, 0.5, 0.5))]
+    if with_boxes:
+        prims.append(Box((0.4, 0.0, 1.0), (1.1, 0.9, 1.8), albedo=(0.0, 1.0, 1.0)))
+        prims.append(Box((2.0, 0.0, 4.2), (2.7, 1.2, 5.0), albedo=(1.0, 0.0, 1.0)))
+    prims.extend(extra)
+    return Scene(primitives=tuple(prims), light=PointLight((w / 2, h - 0.1, l / 2)),
+                 interior_lo=(0.0, 0.0, 0.0), interior_hi=(w, h, l))
+
+
+def acceptance_center():
+    w, h, l = ACCEPTANCE_ROOM
+    return np.array([w / 2, h / 2, l / 2])

@@ -102,3 +102,47 @@ def test_gather_untile_gloo(world, C, W, H):
         p.join(timeout=120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) is True
+
+
+def _rows_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_14624_b200.dist import gather_rows, ray_share
+        n = 1001
+        lo, hi = ray_share(n, world, rank)
+        idx = torch.arange(lo, hi)
+        m = (n + world - 1) // world
+        parts = gather_rows([idx.to(torch.int32),
+                             torch.stack([idx * 1.0, -idx * 1.0], 1)], m)
+        if rank == 0:
+            keep = torch.cat([torch.arange(k * m, k * m + ray_share(n, world, k)[1]
+                                           - ray_share(n, world, k)[0])
+                              for k in range(world)])
+            a = parts[0][keep]
+            b = parts[1][keep]
+            q.put(bool(torch.equal(a, torch.arange(n, dtype=torch.int32)) and
+                       torch.equal(b[:, 0], torch.arange(n) * 1.0)))
+        else:
+            assert parts is None
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_rows_ray_shares_gloo(world):
+    """Ray-batch sharding (C5): contiguous shares padded to ceil(n/world)
+    rows, gathered to rank 0 and trimmed back to input order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=10) is True
