@@ -288,6 +288,21 @@ int lfp_selftest_division(const double* a, const double* b, int64_t n,
                           double* ref, double* fast, uint8_t* took,
                           void* stream);
 
+/* ---- debug instrumentation (bounds-check builds only) ----
+ * The library built with -DLFP_CHECK_BOUNDS=1 (liblfprobe_b200_check.so)
+ * checks every probe-map / direction-table / payload / origin / ray-order
+ * index against its array extent and, when `wcount` (device u32[n_out],
+ * zeroed by the caller) is set, counts the writes of every per-ray output
+ * record -- the evidence that each ray writes exactly its own row
+ * (kernels.py:831-843), standing in for compute-sanitizer, which the GPU
+ * pool does not allow. lfp_debug_bounds resets the violation counter and
+ * installs `wcount` (NULL: no write counting) for later launches on
+ * `device`; lfp_debug_report synchronises the device and returns the number
+ * of failed checks and the site id of the first. Release builds return
+ * LFP_ERR_INVALID from both. */
+int lfp_debug_bounds(int device, uint32_t* wcount, int64_t n_out);
+int lfp_debug_report(int device, uint64_t* violations, int32_t* first_site);
+
 /* ---- input production: GPU ray-cast bake ---- */
 
 /* Analytic primitive: kind 0 = axis-aligned box (a = lo, b = hi), kind 1 =

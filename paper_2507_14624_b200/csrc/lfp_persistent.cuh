@@ -146,6 +146,7 @@ __device__ __forceinline__ void lane_cube(Lane& L, const DevProbes& ps,
 #pragma unroll
     for (int c = 0; c < 8; c++) {
         const int idx = L.base + ((c >> 2) & 1) * ny * nz + ((c >> 1) & 1) * nz + (c & 1);
+        LFP_BCHK(idx, ps.P, 201);
         const double ox = __ldg(ps.origins + 3 * idx + 0) - L.ex;
         const double oy = __ldg(ps.origins + 3 * idx + 1) - L.ey;
         const double oz = __ldg(ps.origins + 3 * idx + 2) - L.ez;
@@ -257,6 +258,7 @@ __device__ __forceinline__ int lane_transition(Lane& L, int state,
             const int c = (L.order >> (4 * L.oi)) & 15;
             const int nyz = g.ny * g.nz;
             L.p = L.base + ((c >> 2) & 1) * nyz + ((c >> 1) & 1) * g.nz + (c & 1);
+            LFP_BCHK(L.p, ps.P, 202);
             L.wx = L.ex - __ldg(ps.origins + 3 * L.p + 0);
             L.wy = L.ey - __ldg(ps.origins + 3 * L.p + 1);
             L.wz = L.ez - __ldg(ps.origins + 3 * L.p + 2);
@@ -269,6 +271,7 @@ __device__ __forceinline__ int lane_transition(Lane& L, int state,
                 int ty = (int)(v * (double)R);
                 if (tx > R - 1) tx = R - 1;
                 if (ty > R - 1) ty = R - 1;
+                LFP_BCHK(tx, R, 203); LFP_BCHK(ty, R, 204);
                 const float st = __ldg(ps.dist_hi + (long long)L.p * R * R + tex_index(tx, ty, R, ps.ts_hi));
                 L.fetches += 1;
                 if (isfinite(st) && (double)st <= L.t1 * (1.0 + g.slack)) {
@@ -345,6 +348,7 @@ __device__ __forceinline__ int lane_lo_step(Lane& L, const DevProbes& ps,
 {
     const int res = ps.r;
     L.fetches += lo_fetches(L.lo.ix, L.lo.iy, res);
+    LFP_BCHK(L.lo.ix, res, 205); LFP_BCHK(L.lo.iy, res, 206);
     const float m_f = __ldg(ps.dil_lo + (long long)L.p * res * res +
                             tex_index(L.lo.ix, L.lo.iy, res, ps.ts_lo));
     if (isfinite(m_f)) {
@@ -371,6 +375,7 @@ __device__ __forceinline__ int lane_hi_step(Lane& L, const DevProbes& ps,
     const int res = ps.R;
     const long long pbase = (long long)L.p * res * res;
     const int ti = L.hi.iy * res + L.hi.ix;
+    LFP_BCHK(L.hi.ix, res, 207); LFP_BCHK(L.hi.iy, res, 208);
     const float stored_f = __ldg(ps.dist_hi + pbase + tex_index(L.hi.ix, L.hi.iy, res, ps.ts_hi));
     L.fetches += 1;
     if (isfinite(stored_f)) {

@@ -22,11 +22,11 @@
 // helpers of lfp_trace.cuh, so outputs are identical to the other schedules
 // and to the reference; only the order of work changes.
 //
-// Ray state between iterations (indexed by input ray id, 64 B):
+// Ray state between iterations (indexed by input ray id, 52 B):
 //   double4 (t_max_i, t_max_j, t_max_k, t_cur)             K:715-738
 //   int4    (ci | cj << 10 | ck << 20, corner order, oi | fetches << 4,
 //            best_p)                                       K:758-799
-//   int4    (best texel tx | ty << 16, -, -, -)            K:795-799, 822
+//   int     best texel tx | ty << 16                       K:795-799, 822
 // t_far and the cube steps are recomputed from the ray each iteration with
 // the reference's own ops (bit-identical).
 #pragma once
@@ -38,8 +38,38 @@ namespace lfp {
 struct WaveState {
     double4* tm;
     int4* cw;
-    int4* bt;
+    int* bt;
 };
+
+// Ray state, ray inputs and queues are touched once per iteration and would
+// otherwise push the probe maps out of L2 (C5: 2^26 rays x ~100 B per
+// iteration vs a 71 MB distance working set): they are read / written with
+// evict-first (.cs) hints; the maps are additionally pinned by an L2
+// access-policy window on the launch (lfp_capi.cu, LFP_WAVE_L2_PERSIST).
+#ifndef LFP_WAVE_STREAMING
+#define LFP_WAVE_STREAMING 1
+#endif
+#if LFP_WAVE_STREAMING
+#define LFP_LDCS(p) __ldcs(p)
+#define LFP_STCS(p, v) __stcs((p), (v))
+#else
+#define LFP_LDCS(p) (*(p))
+#define LFP_STCS(p, v) (*(p) = (v))
+#endif
+
+__device__ __forceinline__ double4 ld_state_cs(const double4* p)
+{
+    const double2* q = reinterpret_cast<const double2*>(p);
+    const double2 a = LFP_LDCS(q), b = LFP_LDCS(q + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ void st_state_cs(double4* p, double4 v)
+{
+    double2* q = reinterpret_cast<double2*>(p);
+    LFP_STCS(q, make_double2(v.x, v.y));
+    LFP_STCS(q + 1, make_double2(v.z, v.w));
+}
 
 struct WaveRays {
     const void* ro;      // origins [n][3] (nullptr: shared eye)
@@ -53,17 +83,21 @@ __device__ __forceinline__ void wave_load_ray(const WaveRays& rays, long long i,
 {
     if (rays.f32) {
         const float* d = (const float*)rays.rd;
-        L.dx = d[3 * i]; L.dy = d[3 * i + 1]; L.dz = d[3 * i + 2];
+        L.dx = LFP_LDCS(d + 3 * i); L.dy = LFP_LDCS(d + 3 * i + 1);
+        L.dz = LFP_LDCS(d + 3 * i + 2);
         if (rays.ro) {
             const float* o = (const float*)rays.ro;
-            L.ex = o[3 * i]; L.ey = o[3 * i + 1]; L.ez = o[3 * i + 2];
+            L.ex = LFP_LDCS(o + 3 * i); L.ey = LFP_LDCS(o + 3 * i + 1);
+            L.ez = LFP_LDCS(o + 3 * i + 2);
         }
     } else {
         const double* d = (const double*)rays.rd;
-        L.dx = d[3 * i]; L.dy = d[3 * i + 1]; L.dz = d[3 * i + 2];
+        L.dx = LFP_LDCS(d + 3 * i); L.dy = LFP_LDCS(d + 3 * i + 1);
+        L.dz = LFP_LDCS(d + 3 * i + 2);
         if (rays.ro) {
             const double* o = (const double*)rays.ro;
-            L.ex = o[3 * i]; L.ey = o[3 * i + 1]; L.ez = o[3 * i + 2];
+            L.ex = LFP_LDCS(o + 3 * i); L.ey = LFP_LDCS(o + 3 * i + 1);
+            L.ez = LFP_LDCS(o + 3 * i + 2);
         }
     }
     if (!rays.ro) { L.ex = rays.eye.x; L.ey = rays.eye.y; L.ez = rays.eye.z; }
@@ -131,7 +165,7 @@ __device__ __forceinline__ int wave_probe(const Lane& L, const GridParams& g)
 // the reference's ops, bit-identical).
 __device__ __forceinline__ void wave_restore(Lane& L, const GridParams& g,
                                              const double4 tm, const int4 cw,
-                                             const int4 bt)
+                                             const int bt)
 {
     L.t_max_i = tm.x; L.t_max_j = tm.y; L.t_max_k = tm.z; L.t_cur = tm.w;
     L.ci = cw.x & 1023; L.cj = (cw.x >> 10) & 1023; L.ck = (cw.x >> 20) & 1023;
@@ -139,8 +173,8 @@ __device__ __forceinline__ void wave_restore(Lane& L, const GridParams& g,
     L.oi = cw.z & 15;
     L.fetches = (int)((unsigned)cw.z >> 4);
     L.best_p = cw.w;
-    L.best_tx = bt.x < 0 ? -1 : (bt.x & 0xFFFF);
-    L.best_ty = bt.x < 0 ? -1 : (bt.x >> 16);
+    L.best_tx = bt < 0 ? -1 : (bt & 0xFFFF);
+    L.best_ty = bt < 0 ? -1 : (bt >> 16);
     const double cell = g.cell;
     L.t_d_i = L.dx != 0.0 ? fabs(cell / L.dx) : CUDART_INF;
     L.t_d_j = L.dy != 0.0 ? fabs(cell / L.dy) : CUDART_INF;
@@ -175,7 +209,7 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
     bool done = false, live = false;
     unsigned key = 0;
     if (valid) {
-        ray = q_in ? __ldg(q_in + i) : (int)i;
+        ray = q_in ? LFP_LDCS(q_in + i) : (int)i;
         wave_load_ray(rays, ray, L);
         L.steps = (L.dx > 0.0 ? 1 : 0) | (L.dy > 0.0 ? 2 : 0) | (L.dz > 0.0 ? 4 : 0);
         bool inside = true;
@@ -202,7 +236,7 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
             L.t0 = (0.0 > tm.w) ? 0.0 : tm.w;
             L.t1 = t_exit_cube;
 #if !LFP_WAVE_RELOAD
-            wave_restore(L, g, tm, cw, S.bt[ray]);
+            wave_restore(L, g, tm, cw, LFP_LDCS(S.bt + ray));
 #endif
         }
         bool requeue = false;
@@ -223,10 +257,12 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                 // above the trace
                 const double4* tmp = S.tm;
                 const int4* cwp = S.cw;
-                const int4* btp = S.bt;
+                const int* btp = S.bt;
                 asm volatile("" : "+l"(tmp), "+l"(cwp), "+l"(btp)
                              : "r"(s.status), "r"(s.fetches));
-                wave_restore(L, g, tmp[ray], cwp[ray], btp[ray]);
+                // last reads of this iteration: evict-first
+                wave_restore(L, g, ld_state_cs(tmp + ray), LFP_LDCS(cwp + ray),
+                             LFP_LDCS(btp + ray));
 #if LFP_WAVE_RELOAD_RAY
                 // the ray too: its origin is dead once the trace has formed
                 // w = e - origin, so it is not kept (spilled) across the trace
@@ -261,13 +297,14 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
         if (requeue) {
             live = true;
             key = wave_key(L, ps, wave_probe(L, g), cbits);
-            S.tm[ray] = make_double4(L.t_max_i, L.t_max_j, L.t_max_k, L.t_cur);
-            S.cw[ray] = make_int4(L.ci | (L.cj << 10) | (L.ck << 20),
-                                  (int)L.order,
-                                  (int)(((unsigned)L.fetches << 4) | (unsigned)L.oi),
-                                  L.best_p);
-            S.bt[ray] = make_int4(L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)),
-                                  0, 0, 0);
+            st_state_cs(S.tm + ray,
+                        make_double4(L.t_max_i, L.t_max_j, L.t_max_k, L.t_cur));
+            LFP_STCS(S.cw + ray,
+                     make_int4(L.ci | (L.cj << 10) | (L.ck << 20), (int)L.order,
+                               (int)(((unsigned)L.fetches << 4) | (unsigned)L.oi),
+                               L.best_p));
+            LFP_STCS(S.bt + ray,
+                     L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)));
         }
     }
     // queue the live rays (warp-aggregated slot allocation)
@@ -280,8 +317,9 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
         base = __shfl_sync(FULL, base, leader);
         if (live) {
             const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
-            key_out[pos] = key;
-            q_out[pos] = ray;
+            LFP_BCHK(pos, n_in, 401);
+            LFP_STCS(key_out + pos, key);
+            LFP_STCS(q_out + pos, ray);
         }
     }
     emit_fn(valid && done, ray, L, dg);

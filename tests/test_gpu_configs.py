@@ -543,6 +543,9 @@ class TestDropInSemantics:
         from paper_2507_14624_b200 import kernels
         z = golden("pcgrid")
         ps = GoldenProbeSet(z)
+        # private copies: the session-scoped golden arrays must stay intact
+        for k in ("dist_hi", "dir_hi", "irr_hi", "dist_lo", "origins"):
+            setattr(ps, k, getattr(ps, k).copy())
         args_tail = (z["grid_origin"], float(z["cell"]),
                      *(int(v) for v in z["dims"]), z["cam_eye"], z["cam_dirs"],
                      1e-4, 1e-4, 1e-3)

@@ -34,6 +34,41 @@ def step(name):
     print(f"[sanitize] {name}", flush=True)
 
 
+# With the bounds-check build (LFP_LIB_PATH=.../liblfprobe_b200_check.so)
+# every call below runs with index checks on and, where the call writes n
+# per-ray records, a write counter per record.
+import ctypes  # noqa: E402
+
+from paper_2507_14624_b200 import native  # noqa: E402
+
+DEBUG = native.lib().lfp_debug_bounds(0, None, 0) == 0
+CHECKED = 0
+
+
+def checked(n, fn, expect=None):
+    """Run fn(); in the check build assert no index violation and that the
+    n output records were written exactly once each (or `expect(result)`
+    times: an int array)."""
+    global CHECKED
+    if not DEBUG:
+        return fn()
+    L = native.lib()
+    wc = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+    native.check(L.lfp_debug_bounds(0, ctypes.c_void_p(wc.data_ptr()), n))
+    r = fn()
+    v, site = ctypes.c_uint64(), ctypes.c_int32()
+    native.check(L.lfp_debug_report(0, ctypes.byref(v), ctypes.byref(site)))
+    native.check(L.lfp_debug_bounds(0, None, 0))
+    assert v.value == 0, f"{v.value} index violations, first at site {site.value}"
+    w = wc.cpu().numpy()[:n]
+    want = np.ones(n, np.int32) if expect is None else np.asarray(expect(r))
+    assert np.array_equal(w, want), \
+        f"write counts: {int((w != want).sum())} of {n} records wrong " \
+        f"(max {int(w.max()) if n else 0})"
+    CHECKED += 1
+    return r
+
+
 def main():
     z = load_golden("pcgrid")
     grid = golden_grid(z)
@@ -43,7 +78,7 @@ def main():
     cam = golden_camera(z, "cam_")
     cam = Camera(eye=cam.eye, forward=cam.forward, up=cam.up,
                  vfov_deg=cam.vfov_deg, width=64, height=48)
-    fr = render_frame(grid, cam)
+    fr = checked(64 * 48, lambda: render_frame(grid, cam))
     res, _ = oracle.render_camera(grid.probe_set, grid.grid_origin,
                                   grid.cell_size, grid.dims, cam)
     assert np.array_equal(fr.status.ravel(), res.status)
@@ -56,16 +91,20 @@ def main():
                             width=64, height=48)]
         full = dev.RayOutputs(2 * 64 * 48, dps.device, probe=True, texel=True,
                               fetch=True, hit_t=True, rgb8=True)
-        dev.render_cameras(dps, g, cams, 64, 48, full)
+        checked(2 * 64 * 48,
+                lambda: dev.render_cameras(dps, g, cams, 64, 48, full))
         T = dev.num_tiles(2, 64, 48)
         parts_s, parts_c = [], []
         for k in range(3):
             nk = (T - k + 2) // 3
             o = dev.RayOutputs(((T + 2) // 3) * 128, dps.device)
-            o.status.zero_()
+            o.status.fill_(255)
             o.rgb.zero_()
-            dev.render_cameras(dps, g, cams, 64, 48, o, tile_begin=k,
-                               tile_step=3, n_tiles=nk, compact=True)
+            checked(o.n, lambda: dev.render_cameras(
+                dps, g, cams, 64, 48, o, tile_begin=k, tile_step=3,
+                n_tiles=nk, compact=True),
+                expect=lambda _: (o.status != 255).int().cpu().numpy())
+            o.status[o.status == 255] = 0
             parts_s.append(o.status)
             parts_c.append(o.rgb)
         st = torch.empty(2 * 64 * 48, dtype=torch.uint8, device="cuda")
@@ -79,15 +118,16 @@ def main():
     g = dev.grid_params(grid.grid_origin, grid.cell_size, grid.dims,
                         DEFAULT_CONFIG, mode="check")
     o = dev.RayOutputs(64 * 48, dps.device, diag=True)
-    dev.render_cameras(dps, g, [cam], 64, 48, o)
+    checked(64 * 48, lambda: dev.render_cameras(dps, g, [cam], 64, 48, o))
     torch.cuda.synchronize()
     assert int(o.diag[4]) == 0
 
     step("hierarchy (two levels of different resolution)")
     c1 = configs.c1()
     h = ProbeHierarchy([c1.grid, grid])
-    frh = render_frame(h, Camera(eye=(1.3, 1.1, 1.7), forward=(0.4, -0.2, -1.0),
-                                 width=40, height=24))
+    frh = checked(40 * 24, lambda: render_frame(
+        h, Camera(eye=(1.3, 1.1, 1.7), forward=(0.4, -0.2, -1.0), width=40,
+                  height=24)))
     assert frh.status.shape == (24, 40)
 
     o32 = z["inc_origins"][:1024].astype(np.float64)
@@ -106,9 +146,10 @@ def main():
             out.rgb.zero_()
             if binned:
                 order = dev.ray_order(dev.bin_rays(g, to, td))
-                dev.trace_rays_ordered(dps, g, to, td, order, out)
+                checked(1024, lambda: dev.trace_rays_ordered(
+                    dps, g, to, td, order, out))
             else:
-                dev.trace_rays(dps, g, to, td, out)
+                checked(1024, lambda: dev.trace_rays(dps, g, to, td, out))
             torch.cuda.synchronize()
             assert np.array_equal(out.status.cpu().numpy(), exp.status)
             assert np.array_equal(out.fetch.cpu().numpy(), exp.fetch)
@@ -117,7 +158,7 @@ def main():
     g = dev.grid_params(grid.grid_origin, grid.cell_size, grid.dims,
                         DEFAULT_CONFIG)
     out = dev.RayOutputs(1024, dps.device, fetch=True)
-    dev.render_grid_dirs(dps, g, o32[0], td.float(), out)
+    checked(1024, lambda: dev.render_grid_dirs(dps, g, o32[0], td.float(), out))
     torch.cuda.synchronize()
 
     step("non-grid sources: single probe, probe list, eye-aligned lookup")
@@ -136,7 +177,7 @@ def main():
         c = golden_camera(zm, name + "_")
         c = Camera(eye=c.eye, forward=c.forward, up=c.up, vfov_deg=c.vfov_deg,
                    width=48, height=32)
-        render_frame(src, c)
+        checked(48 * 32, lambda: render_frame(src, c))
 
     step("ray-cast bake (lfp_bake_probes)")
     bake_grid_gpu(c1.scene, (0.0, 0.0, 0.0), 4.0, (2, 2, 2), 32, 8, quant="f16")
@@ -161,6 +202,19 @@ def main():
         ctypes.c_void_p(took.data_ptr()),
         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
+    if DEBUG:
+        step("C5-like wavefront batch at 2^20 rays (default schedule)")
+        o5, d5 = configs.c5_rays(c1.scene, 1 << 20, seed=3)
+        t5o, t5d = torch.from_numpy(o5).cuda(), torch.from_numpy(d5).cuda()
+        g = dev.grid_params(c1.grid.grid_origin, c1.grid.cell_size,
+                            c1.grid.dims, DEFAULT_CONFIG)
+        out = dev.RayOutputs(1 << 20, dps.device, probe=True, texel=True,
+                             fetch=True, hit_t=True)
+        c1dps = device_probe_set(c1.grid)
+        checked(1 << 20, lambda: dev.trace_rays(c1dps, g, t5o, t5d, out))
+        print(f"[sanitize] bounds-check build: {CHECKED} checked calls, 0 "
+              "index violations, every output record written exactly once",
+              flush=True)
     print("[sanitize] all kernel families ran", flush=True)
 
 
