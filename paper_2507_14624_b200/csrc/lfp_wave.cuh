@@ -127,6 +127,12 @@ __device__ __forceinline__ void wave_oct_cell(float x, float y, float z,
     cv = v < 0 ? 0 : (v > hi ? hi : v);
 }
 
+#ifndef LFP_WAVE_KEY_LEN
+#define LFP_WAVE_KEY_LEN 0
+#endif
+#ifndef LFP_WAVE_KEY_NSEG
+#define LFP_WAVE_KEY_NSEG 0
+#endif
 __device__ __forceinline__ unsigned wave_key(const Lane& L, const DevProbes& ps,
                                              int p, int cbits)
 {
@@ -139,13 +145,35 @@ __device__ __forceinline__ unsigned wave_key(const Lane& L, const DevProbes& ps,
     const float scale = (float)(1 << cbits);
     const int hi = (1 << cbits) - 1;
     int c[4];
-    wave_oct_cell(ex + t0 * dx, ey + t0 * dy, ez + t0 * dz, scale, hi, c[0], c[1]);
-    wave_oct_cell(ex + t1 * dx, ey + t1 * dy, ez + t1 * dz, scale, hi, c[2], c[3]);
+    const float x0 = ex + t0 * dx, y0 = ey + t0 * dy, z0 = ez + t0 * dz;
+    const float x1 = ex + t1 * dx, y1 = ey + t1 * dy, z1 = ez + t1 * dz;
+    wave_oct_cell(x0, y0, z0, scale, hi, c[0], c[1]);
+    wave_oct_cell(x1, y1, z1, scale, hi, c[2], c[3]);
     unsigned m = 0;
     for (int b = cbits - 1; b >= 0; b--)
 #pragma unroll
         for (int k = 0; k < 4; k++) m = (m << 1) | ((unsigned)(c[k] >> b) & 1u);
+#if LFP_WAVE_KEY_LEN
+    // chord length in cells (Manhattan, halved, 5 bits) above the cell code:
+    // a warp's lanes then walk about the same number of low-res blocks
+    {
+        const int sh = cbits > 5 ? cbits - 5 : 0;   // measure at <= 32 cells/axis
+        int len = (abs((c[2] >> sh) - (c[0] >> sh)) + abs((c[3] >> sh) - (c[1] >> sh)));
+        len = len > 31 ? 31 : len;
+        return ((((unsigned)p << 5) | (unsigned)len) << (4 * cbits)) | m;
+    }
+#elif LFP_WAVE_KEY_NSEG
+    // fold crossings of the range (K:102-129: one per axis whose probe-space
+    // coordinate changes sign) = segments - 1, above the cell code: a warp's
+    // lanes then run the same number of segments (a probe range has 1-4; with
+    // mixed lanes the warp runs the longest count with the others idle)
+    const unsigned nx = (unsigned)((x0 < 0.0f) != (x1 < 0.0f)) +
+                        (unsigned)((y0 < 0.0f) != (y1 < 0.0f)) +
+                        (unsigned)((z0 < 0.0f) != (z1 < 0.0f));
+    return ((((unsigned)p << 2) | nx) << (4 * cbits)) | m;
+#else
     return ((unsigned)p << (4 * cbits)) | m;
+#endif
 }
 
 __device__ __forceinline__ int wave_probe(const Lane& L, const GridParams& g)
