@@ -22,11 +22,22 @@
 // helpers of lfp_trace.cuh, so outputs are identical to the other schedules
 // and to the reference; only the order of work changes.
 //
-// Ray state between iterations (indexed by input ray id, 52 B):
-//   double4 (t_max_i, t_max_j, t_max_k, t_cur)             K:715-738
-//   int4    (ci | cj << 10 | ck << 20, corner order, oi | fetches << 4,
-//            best_p)                                       K:758-799
-//   int     best texel tx | ty << 16                       K:795-799, 822
+// Ray state between iterations: ONE record per ray, indexed by input ray id
+// (LFP_WAVE_PACKED; 96 B for f32 rays, 128 B for f64 rays):
+//   [0, R)        origin, direction (f32 x6 + pad / f64 x6 + pad), written
+//                 once when the ray enters the lattice
+//   [S-64, S-32)  double4 (t_max_i, t_max_j, t_max_k, t_cur)    K:715-738
+//   [S-32, S-16)  int4 (ci | cj << 10 | ck << 20, corner order,
+//                 oi | fetches << 4, best_p)                    K:758-799
+//   [S-16, S-12)  best texel tx | ty << 16                      K:795-799, 822
+// A re-queued ray is gathered by ray id (the queue is sorted by probe and
+// chord, so the ids are random): with separate arrays for origins,
+// directions and the three state parts that was five 64-byte DRAM fetches
+// per ray and iteration, most of them for 4-16 useful bytes, plus partial-
+// sector writes that L2 has to fill first -- the bulk of the wavefront's
+// DRAM traffic (ncu: 955 B per probe trace, ~2x the algorithmic bytes). The
+// packed record is two fetches and one 64-byte full-sector write-back; the
+// input ray arrays are read once (coalesced) by the first iteration.
 // t_far and the cube steps are recomputed from the ray each iteration with
 // the reference's own ops (bit-identical).
 #pragma once
@@ -35,10 +46,19 @@
 
 namespace lfp {
 
+#ifndef LFP_WAVE_PACKED
+#define LFP_WAVE_PACKED 1
+#endif
+
 struct WaveState {
+#if LFP_WAVE_PACKED
+    char* rec;      // [n][stride]
+    int stride;     // 96 (f32 rays) or 128 (f64 rays)
+#else
     double4* tm;
     int4* cw;
     int* bt;
+#endif
 };
 
 // Ray state, ray inputs and queues are touched once per iteration and would
@@ -71,6 +91,32 @@ __device__ __forceinline__ void st_state_cs(double4* p, double4 v)
     LFP_STCS(q + 1, make_double2(v.z, v.w));
 }
 
+#if LFP_WAVE_PACKED
+__device__ __forceinline__ char* wave_rec(const WaveState& S, long long ray)
+{
+    return S.rec + ray * (long long)S.stride;
+}
+// the mutable 64 bytes of a record
+__device__ __forceinline__ void wave_ld_mut(const char* r, int stride, double4& tm,
+                                            int4& cw, int& bt)
+{
+    const char* m = r + stride - 64;
+    tm = ld_state_cs(reinterpret_cast<const double4*>(m));
+    const int4 a = LFP_LDCS(reinterpret_cast<const int4*>(m + 32));
+    const int4 b = LFP_LDCS(reinterpret_cast<const int4*>(m + 48));
+    cw = a;
+    bt = b.x;
+}
+__device__ __forceinline__ void wave_st_mut(char* r, int stride, double4 tm, int4 cw,
+                                            int bt)
+{
+    char* m = r + stride - 64;
+    st_state_cs(reinterpret_cast<double4*>(m), tm);
+    LFP_STCS(reinterpret_cast<int4*>(m + 32), cw);
+    LFP_STCS(reinterpret_cast<int4*>(m + 48), make_int4(bt, 0, 0, 0));
+}
+#endif
+
 struct WaveRays {
     const void* ro;      // origins [n][3] (nullptr: shared eye)
     const void* rd;      // directions [n][3]
@@ -102,6 +148,38 @@ __device__ __forceinline__ void wave_load_ray(const WaveRays& rays, long long i,
     }
     if (!rays.ro) { L.ex = rays.eye.x; L.ey = rays.eye.y; L.ez = rays.eye.z; }
 }
+
+#if LFP_WAVE_PACKED
+// origin / direction of a re-queued ray from its record (exact copies of the
+// input values; f32 inputs are widened exactly as wave_load_ray does)
+__device__ __forceinline__ void wave_ld_ray(const char* r, int f32, Lane& L)
+{
+    if (f32) {
+        const float4 a = LFP_LDCS(reinterpret_cast<const float4*>(r));
+        const float2 b = LFP_LDCS(reinterpret_cast<const float2*>(r + 16));
+        L.ex = a.x; L.ey = a.y; L.ez = a.z; L.dx = a.w; L.dy = b.x; L.dz = b.y;
+    } else {
+        const double2 a = LFP_LDCS(reinterpret_cast<const double2*>(r));
+        const double2 b = LFP_LDCS(reinterpret_cast<const double2*>(r + 16));
+        const double2 c = LFP_LDCS(reinterpret_cast<const double2*>(r + 32));
+        L.ex = a.x; L.ey = a.y; L.ez = b.x; L.dx = b.y; L.dy = c.x; L.dz = c.y;
+    }
+}
+__device__ __forceinline__ void wave_st_ray(char* r, int f32, const Lane& L)
+{
+    if (f32) {
+        LFP_STCS(reinterpret_cast<float4*>(r),
+                 make_float4((float)L.ex, (float)L.ey, (float)L.ez, (float)L.dx));
+        LFP_STCS(reinterpret_cast<float4*>(r + 16),
+                 make_float4((float)L.dy, (float)L.dz, 0.0f, 0.0f));
+    } else {
+        LFP_STCS(reinterpret_cast<double2*>(r), make_double2(L.ex, L.ey));
+        LFP_STCS(reinterpret_cast<double2*>(r + 16), make_double2(L.ez, L.dx));
+        LFP_STCS(reinterpret_cast<double2*>(r + 32), make_double2(L.dy, L.dz));
+        LFP_STCS(reinterpret_cast<double2*>(r + 48), make_double2(0.0, 0.0));
+    }
+}
+#endif
 
 // Sort key of a re-queued ray (scheduling only, never a result): the next
 // probe p, then a 4-D Morton code of the octahedral cells (2^cbits per axis)
@@ -186,7 +264,7 @@ __device__ __forceinline__ int wave_probe(const Lane& L, const GridParams& g)
 #define LFP_WAVE_RELOAD 1
 #endif
 #ifndef LFP_WAVE_RELOAD_RAY
-#define LFP_WAVE_RELOAD_RAY 0
+#define LFP_WAVE_RELOAD_RAY 1
 #endif
 
 // The walk state of a re-queued ray (K:715-738 increments recomputed with
@@ -238,7 +316,12 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
     unsigned key = 0;
     if (valid) {
         ray = q_in ? LFP_LDCS(q_in + i) : (int)i;
+#if LFP_WAVE_PACKED
+        if (first) wave_load_ray(rays, ray, L);
+        else wave_ld_ray(wave_rec(S, ray), rays.f32, L);
+#else
         wave_load_ray(rays, ray, L);
+#endif
         L.steps = (L.dx > 0.0 ? 1 : 0) | (L.dy > 0.0 ? 2 : 0) | (L.dz > 0.0 ? 4 : 0);
         bool inside = true;
         if (first) {
@@ -251,8 +334,15 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
             // memory -- across the trace's loops.
             double t_near;
             lattice_slab(g, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, t_near, L.t_far);
+#if LFP_WAVE_PACKED
+            double4 tm;
+            int4 cw;
+            int bt0;
+            wave_ld_mut(wave_rec(S, ray), S.stride, tm, cw, bt0);
+#else
             const double4 tm = S.tm[ray];
             const int4 cw = S.cw[ray];
+#endif
             L.ci = cw.x & 1023; L.cj = (cw.x >> 10) & 1023; L.ck = (cw.x >> 20) & 1023;
             L.order = (unsigned)cw.y;
             L.oi = cw.z & 15;
@@ -264,7 +354,11 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
             L.t0 = (0.0 > tm.w) ? 0.0 : tm.w;
             L.t1 = t_exit_cube;
 #if !LFP_WAVE_RELOAD
+#if LFP_WAVE_PACKED
+            wave_restore(L, g, tm, cw, bt0);
+#else
             wave_restore(L, g, tm, cw, LFP_LDCS(S.bt + ray));
+#endif
 #endif
         }
         bool requeue = false;
@@ -283,6 +377,19 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                 // opaque copies that depend on the trace's result: the
                 // compiler can neither reuse the loads above nor hoist these
                 // above the trace
+#if LFP_WAVE_PACKED
+                const char* rp = wave_rec(S, ray);
+                asm volatile("" : "+l"(rp) : "r"(s.status), "r"(s.fetches));
+                double4 tm2;
+                int4 cw2;
+                int bt2;
+                // last reads of this iteration: evict-first
+                wave_ld_mut(rp, S.stride, tm2, cw2, bt2);
+                wave_restore(L, g, tm2, cw2, bt2);
+#if LFP_WAVE_RELOAD_RAY
+                wave_ld_ray(rp, rays.f32, L);
+#endif
+#else
                 const double4* tmp = S.tm;
                 const int4* cwp = S.cw;
                 const int* btp = S.bt;
@@ -291,7 +398,8 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                 // last reads of this iteration: evict-first
                 wave_restore(L, g, ld_state_cs(tmp + ray), LFP_LDCS(cwp + ray),
                              LFP_LDCS(btp + ray));
-#if LFP_WAVE_RELOAD_RAY
+#endif
+#if LFP_WAVE_RELOAD_RAY && !LFP_WAVE_PACKED
                 // the ray too: its origin is dead once the trace has formed
                 // w = e - origin, so it is not kept (spilled) across the trace
                 WaveRays rr = rays;
@@ -325,6 +433,16 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
         if (requeue) {
             live = true;
             key = wave_key(L, ps, wave_probe(L, g), cbits);
+#if LFP_WAVE_PACKED
+            char* rp = wave_rec(S, ray);
+            if (first) wave_st_ray(rp, rays.f32, L);
+            wave_st_mut(rp, S.stride,
+                        make_double4(L.t_max_i, L.t_max_j, L.t_max_k, L.t_cur),
+                        make_int4(L.ci | (L.cj << 10) | (L.ck << 20), (int)L.order,
+                                  (int)(((unsigned)L.fetches << 4) | (unsigned)L.oi),
+                                  L.best_p),
+                        L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)));
+#else
             st_state_cs(S.tm + ray,
                         make_double4(L.t_max_i, L.t_max_j, L.t_max_k, L.t_cur));
             LFP_STCS(S.cw + ray,
@@ -333,6 +451,7 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                                L.best_p));
             LFP_STCS(S.bt + ray,
                      L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)));
+#endif
         }
     }
     // queue the live rays (warp-aggregated slot allocation)
