@@ -1,0 +1,7 @@
+out=gpurun_out/r02r; mkdir -p $out
+V=build/variants
+bash tools/ab.sh "c3 c2 c5 c4" $V/liblfprobe_b200_LFP_RADII_T0.so $V/liblfprobe_b200_LFP_RADII_T1.so 2>&1 | tee $out/ab_radii_t.txt
+python tools/diag.py c3 > $out/diag_c3.json 2>&1
+python tools/diag.py c2 > $out/diag_c2.json 2>&1
+python tools/diag_c5.py > $out/diag_c5.json 2>&1
+python -m pytest tests -m gpu -q -x > $out/pytest_gpu.log 2>&1; tail -3 $out/pytest_gpu.log
