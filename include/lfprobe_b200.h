@@ -288,6 +288,14 @@ int lfp_selftest_division(const double* a, const double* b, int64_t n,
                           double* ref, double* fast, uint8_t* took,
                           void* stream);
 
+/* The same for the high-res DDA set-up's division (dda_init_hi): a / b
+ * formed from the correctly rounded reciprocal of b, obtained by the exact
+ * power-of-two scaling (1 / (b / 4)) / 4 the tracer applies to the low-res
+ * DDA increments. */
+int lfp_selftest_division_recip(const double* a, const double* b, int64_t n,
+                                double* ref, double* fast, uint8_t* took,
+                                void* stream);
+
 /* ---- debug instrumentation (bounds-check builds only) ----
  * The library built with -DLFP_CHECK_BOUNDS=1 (liblfprobe_b200_check.so)
  * checks every probe-map / direction-table / payload / origin / ray-order

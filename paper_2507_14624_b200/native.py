@@ -125,6 +125,7 @@ def lib():
             vp, ctypes.POINTER(GridParams), vp, vp, i32, i64, vp,
             ctypes.POINTER(Outputs), vp]
         L.lfp_selftest_division.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+        L.lfp_selftest_division_recip.argtypes = [vp, vp, i64, vp, vp, vp, vp]
         L.lfp_debug_bounds.argtypes = [ctypes.c_int, vp, i64]
         L.lfp_debug_report.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
                                        ctypes.POINTER(i32)]
@@ -135,7 +136,8 @@ def lib():
         L.lfp_bake_points.argtypes = [
             ctypes.c_int, vp, vp, i64, vp, i64, i32, i32, u32, vp, vp, vp, vp,
             vp, vp]
-        for name in ("lfp_selftest_division", "lfp_debug_bounds",
+        for name in ("lfp_selftest_division", "lfp_selftest_division_recip",
+                     "lfp_debug_bounds",
                      "lfp_debug_report", "lfp_bake_points", "lfp_render_hierarchy", "lfp_probeset_create_packed",
                      "lfp_render_frame_host",
                      "lfp_bin_rays", "lfp_trace_rays_ordered",
@@ -163,4 +165,5 @@ def exported_symbols():
             "lfp_bin_rays", "lfp_trace_rays_ordered",
             "lfp_probeset_create_packed", "lfp_render_hierarchy",
             "lfp_bake_points", "lfp_last_launches", "lfp_render_frame_host",
-            "lfp_selftest_division", "lfp_debug_bounds", "lfp_debug_report"]
+            "lfp_selftest_division", "lfp_selftest_division_recip",
+            "lfp_debug_bounds", "lfp_debug_report"]

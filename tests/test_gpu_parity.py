@@ -650,7 +650,9 @@ class TestPersistentSchedule:
 
 
 @pytest.mark.gpu
-def test_branch_free_division_is_ieee():
+@pytest.mark.parametrize("entry", ["lfp_selftest_division",
+                                   "lfp_selftest_division_recip"])
+def test_branch_free_division_is_ieee(entry):
     """The tracer's branch-free division (rcp_nv / div_nv, LFP_FAST_DIV)
     equals nvcc's IEEE `a / b` bit for bit whenever its fast-path test
     passes (and falls back to `a / b` otherwise): random operands over the
@@ -676,7 +678,7 @@ def test_branch_free_division_is_ieee():
     fast = torch.empty_like(ta)
     took = torch.empty(len(a), dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
-    native.check(native.lib().lfp_selftest_division(
+    native.check(getattr(native.lib(), entry)(
         ctypes.c_void_p(ta.data_ptr()), ctypes.c_void_p(tb.data_ptr()), len(a),
         ctypes.c_void_p(ref.data_ptr()), ctypes.c_void_p(fast.data_ptr()),
         ctypes.c_void_p(took.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
