@@ -494,11 +494,13 @@ def e2e_measure(wl, steps, world, rank, local):
     if wl.name == "c5":
         from paper_2507_14624_b200 import configs
         if world == 1:
-            o_h = wl.o.cpu().numpy()
-            d_h = wl.d.cpu().numpy()
+            # the step's inputs live in page-locked host memory (contract)
+            o_pin = wl.o.cpu().pin_memory()
+            d_pin = wl.d.cpu().pin_memory()
+            o_h, d_h = o_pin.numpy(), d_pin.numpy()
             call = lambda: pkg.trace_rays(wl.cfg.grid, o_h, d_h, device=local)  # noqa: E731
-            api = ("trace_rays(ProbeGrid, origins, dirs) host f32 arrays -> "
-                   "host results")
+            api = ("trace_rays(ProbeGrid, origins, dirs) page-locked host f32 "
+                   "arrays -> host results")
         else:
             o_h, d_h = configs.c5_rays(wl.cfg.scene, C5_RAYS)
             call = lambda: pdist.trace_rays_sharded(  # noqa: E731

@@ -227,10 +227,17 @@ __device__ __forceinline__ unsigned wave_key(const Lane& L, const DevProbes& ps,
     const float x1 = ex + t1 * dx, y1 = ey + t1 * dy, z1 = ez + t1 * dz;
     wave_oct_cell(x0, y0, z0, scale, hi, c[0], c[1]);
     wave_oct_cell(x1, y1, z1, scale, hi, c[2], c[3]);
+    // 4-D Morton code: bit b of coordinate k lands at 4 b + (3 - k); each
+    // coordinate (<= 8 bits) is spread by three shift-or-mask steps
     unsigned m = 0;
-    for (int b = cbits - 1; b >= 0; b--)
 #pragma unroll
-        for (int k = 0; k < 4; k++) m = (m << 1) | ((unsigned)(c[k] >> b) & 1u);
+    for (int k = 0; k < 4; k++) {
+        unsigned x = (unsigned)c[k] & 0xffu;
+        x = (x | (x << 12)) & 0x000f000fu;
+        x = (x | (x << 6)) & 0x03030303u;
+        x = (x | (x << 3)) & 0x11111111u;
+        m |= x << (3 - k);
+    }
 #if LFP_WAVE_KEY_LEN
     // chord length in cells (Manhattan, halved, 5 bits) above the cell code:
     // a warp's lanes then walk about the same number of low-res blocks
