@@ -23,13 +23,14 @@
 // and to the reference; only the order of work changes.
 //
 // Ray state between iterations: ONE record per ray, indexed by input ray id
-// (LFP_WAVE_PACKED; 96 B for f32 rays, 128 B for f64 rays):
+// (96 B for f32 rays, 128 B for f64 rays):
 //   [0, R)        origin, direction (f32 x6 + pad / f64 x6 + pad), written
 //                 once when the ray enters the lattice
 //   [S-64, S-32)  double4 (t_max_i, t_max_j, t_max_k, t_cur)    K:715-738
 //   [S-32, S-16)  int4 (ci | cj << 10 | ck << 20, corner order,
 //                 oi | fetches << 4, best_p)                    K:758-799
 //   [S-16, S-12)  best texel tx | ty << 16                      K:795-799, 822
+//   [S-8, S)      t_far, the ray's exit from the lattice        K:668-692
 // A re-queued ray is gathered by ray id (the queue is sorted by probe and
 // chord, so the ids are random): with separate arrays for origins,
 // directions and the three state parts that was five 64-byte DRAM fetches
@@ -38,27 +39,17 @@
 // DRAM traffic (ncu: 955 B per probe trace, ~2x the algorithmic bytes). The
 // packed record is two fetches and one 64-byte full-sector write-back; the
 // input ray arrays are read once (coalesced) by the first iteration.
-// t_far and the cube steps are recomputed from the ray each iteration with
-// the reference's own ops (bit-identical).
+// The cube increment |cell / d| is recomputed (reference ops, bit-identical)
+// only when a ray moves to the next cube.
 #pragma once
 
 #include "lfp_persistent.cuh"
 
 namespace lfp {
 
-#ifndef LFP_WAVE_PACKED
-#define LFP_WAVE_PACKED 1
-#endif
-
 struct WaveState {
-#if LFP_WAVE_PACKED
     char* rec;      // [n][stride]
     int stride;     // 96 (f32 rays) or 128 (f64 rays)
-#else
-    double4* tm;
-    int4* cw;
-    int* bt;
-#endif
 };
 
 // Ray state, ray inputs and queues are touched once per iteration and would
@@ -91,14 +82,13 @@ __device__ __forceinline__ void st_state_cs(double4* p, double4 v)
     LFP_STCS(q + 1, make_double2(v.z, v.w));
 }
 
-#if LFP_WAVE_PACKED
 __device__ __forceinline__ char* wave_rec(const WaveState& S, long long ray)
 {
     return S.rec + ray * (long long)S.stride;
 }
 // the mutable 64 bytes of a record
 __device__ __forceinline__ void wave_ld_mut(const char* r, int stride, double4& tm,
-                                            int4& cw, int& bt)
+                                            int4& cw, int& bt, double& t_far)
 {
     const char* m = r + stride - 64;
     tm = ld_state_cs(reinterpret_cast<const double4*>(m));
@@ -106,16 +96,17 @@ __device__ __forceinline__ void wave_ld_mut(const char* r, int stride, double4& 
     const int4 b = LFP_LDCS(reinterpret_cast<const int4*>(m + 48));
     cw = a;
     bt = b.x;
+    t_far = __hiloint2double(b.w, b.z);
 }
 __device__ __forceinline__ void wave_st_mut(char* r, int stride, double4 tm, int4 cw,
-                                            int bt)
+                                            int bt, double t_far)
 {
     char* m = r + stride - 64;
     st_state_cs(reinterpret_cast<double4*>(m), tm);
     LFP_STCS(reinterpret_cast<int4*>(m + 32), cw);
-    LFP_STCS(reinterpret_cast<int4*>(m + 48), make_int4(bt, 0, 0, 0));
+    LFP_STCS(reinterpret_cast<int4*>(m + 48),
+             make_int4(bt, 0, __double2loint(t_far), __double2hiint(t_far)));
 }
-#endif
 
 struct WaveRays {
     const void* ro;      // origins [n][3] (nullptr: shared eye)
@@ -149,7 +140,6 @@ __device__ __forceinline__ void wave_load_ray(const WaveRays& rays, long long i,
     if (!rays.ro) { L.ex = rays.eye.x; L.ey = rays.eye.y; L.ez = rays.eye.z; }
 }
 
-#if LFP_WAVE_PACKED
 // origin / direction of a re-queued ray from its record (exact copies of the
 // input values; f32 inputs are widened exactly as wave_load_ray does)
 __device__ __forceinline__ void wave_ld_ray(const char* r, int f32, Lane& L)
@@ -179,7 +169,6 @@ __device__ __forceinline__ void wave_st_ray(char* r, int f32, const Lane& L)
         LFP_STCS(reinterpret_cast<double2*>(r + 48), make_double2(0.0, 0.0));
     }
 }
-#endif
 
 // Sort key of a re-queued ray (scheduling only, never a result): the next
 // probe p, then a 4-D Morton code of the octahedral cells (2^cbits per axis)
@@ -288,11 +277,20 @@ __device__ __forceinline__ void wave_restore(Lane& L, const GridParams& g,
     L.best_p = cw.w;
     L.best_tx = bt < 0 ? -1 : (bt & 0xFFFF);
     L.best_ty = bt < 0 ? -1 : (bt >> 16);
-    const double cell = g.cell;
-    L.t_d_i = L.dx != 0.0 ? fabs(cell / L.dx) : CUDART_INF;
-    L.t_d_j = L.dy != 0.0 ? fabs(cell / L.dy) : CUDART_INF;
-    L.t_d_k = L.dz != 0.0 ? fabs(cell / L.dz) : CUDART_INF;
     L.base = (L.ci * g.ny + L.cj) * g.nz + L.ck;
+}
+
+// K:801-821 for a re-queued ray: the increment of the axis that steps
+// (K:715-738, |cell / d|, the reference's own division) is formed here, once
+// per cube change, instead of all three on every iteration.
+__device__ __forceinline__ bool wave_next_cube(Lane& L, const GridParams& g)
+{
+    const int ax = (L.t_max_i <= L.t_max_j && L.t_max_i <= L.t_max_k) ? 0
+                   : (L.t_max_j <= L.t_max_k ? 1 : 2);
+    const double d = ax == 0 ? L.dx : (ax == 1 ? L.dy : L.dz);
+    const double td = d != 0.0 ? fabs(g.cell / d) : CUDART_INF;
+    L.t_d_i = td; L.t_d_j = td; L.t_d_k = td;
+    return lane_next_cube(L, g);
 }
 
 // One iteration for the rays q_in[0..n_in) (q_in == nullptr: identity).
@@ -323,12 +321,8 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
     unsigned key = 0;
     if (valid) {
         ray = q_in ? LFP_LDCS(q_in + i) : (int)i;
-#if LFP_WAVE_PACKED
         if (first) wave_load_ray(rays, ray, L);
         else wave_ld_ray(wave_rec(S, ray), rays.f32, L);
-#else
-        wave_load_ray(rays, ray, L);
-#endif
         L.steps = (L.dx > 0.0 ? 1 : 0) | (L.dy > 0.0 ? 2 : 0) | (L.dz > 0.0 ? 4 : 0);
         bool inside = true;
         if (first) {
@@ -339,17 +333,10 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
             // K:603-605); the rest of the walk state is re-read after the
             // trace (LFP_WAVE_RELOAD) so it is not live -- spilled to local
             // memory -- across the trace's loops.
-            double t_near;
-            lattice_slab(g, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, t_near, L.t_far);
-#if LFP_WAVE_PACKED
             double4 tm;
             int4 cw;
             int bt0;
-            wave_ld_mut(wave_rec(S, ray), S.stride, tm, cw, bt0);
-#else
-            const double4 tm = S.tm[ray];
-            const int4 cw = S.cw[ray];
-#endif
+            wave_ld_mut(wave_rec(S, ray), S.stride, tm, cw, bt0, L.t_far);
             L.ci = cw.x & 1023; L.cj = (cw.x >> 10) & 1023; L.ck = (cw.x >> 20) & 1023;
             L.order = (unsigned)cw.y;
             L.oi = cw.z & 15;
@@ -361,11 +348,7 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
             L.t0 = (0.0 > tm.w) ? 0.0 : tm.w;
             L.t1 = t_exit_cube;
 #if !LFP_WAVE_RELOAD
-#if LFP_WAVE_PACKED
             wave_restore(L, g, tm, cw, bt0);
-#else
-            wave_restore(L, g, tm, cw, LFP_LDCS(S.bt + ray));
-#endif
 #endif
         }
         bool requeue = false;
@@ -384,34 +367,16 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                 // opaque copies that depend on the trace's result: the
                 // compiler can neither reuse the loads above nor hoist these
                 // above the trace
-#if LFP_WAVE_PACKED
                 const char* rp = wave_rec(S, ray);
                 asm volatile("" : "+l"(rp) : "r"(s.status), "r"(s.fetches));
                 double4 tm2;
                 int4 cw2;
                 int bt2;
                 // last reads of this iteration: evict-first
-                wave_ld_mut(rp, S.stride, tm2, cw2, bt2);
+                wave_ld_mut(rp, S.stride, tm2, cw2, bt2, L.t_far);
                 wave_restore(L, g, tm2, cw2, bt2);
 #if LFP_WAVE_RELOAD_RAY
                 wave_ld_ray(rp, rays.f32, L);
-#endif
-#else
-                const double4* tmp = S.tm;
-                const int4* cwp = S.cw;
-                const int* btp = S.bt;
-                asm volatile("" : "+l"(tmp), "+l"(cwp), "+l"(btp)
-                             : "r"(s.status), "r"(s.fetches));
-                // last reads of this iteration: evict-first
-                wave_restore(L, g, ld_state_cs(tmp + ray), LFP_LDCS(cwp + ray),
-                             LFP_LDCS(btp + ray));
-#endif
-#if LFP_WAVE_RELOAD_RAY && !LFP_WAVE_PACKED
-                // the ray too: its origin is dead once the trace has formed
-                // w = e - origin, so it is not kept (spilled) across the trace
-                WaveRays rr = rays;
-                asm volatile("" : "+l"(rr.rd), "+l"(rr.ro) : "r"(s.status));
-                wave_load_ray(rr, ray, L);
 #endif
             }
 #endif
@@ -426,7 +391,7 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                 }
                 L.oi++;
                 if (L.oi == 8) {
-                    if (lane_next_cube(L, g)) {
+                    if (wave_next_cube(L, g)) {
                         lane_cube(L, ps, g);
                     } else {
                         L.status = MISS; L.rp = L.best_p; L.rtx = L.best_tx;
@@ -440,7 +405,6 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
         if (requeue) {
             live = true;
             key = wave_key(L, ps, wave_probe(L, g), cbits);
-#if LFP_WAVE_PACKED
             char* rp = wave_rec(S, ray);
             if (first) wave_st_ray(rp, rays.f32, L);
             wave_st_mut(rp, S.stride,
@@ -448,17 +412,8 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                         make_int4(L.ci | (L.cj << 10) | (L.ck << 20), (int)L.order,
                                   (int)(((unsigned)L.fetches << 4) | (unsigned)L.oi),
                                   L.best_p),
-                        L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)));
-#else
-            st_state_cs(S.tm + ray,
-                        make_double4(L.t_max_i, L.t_max_j, L.t_max_k, L.t_cur));
-            LFP_STCS(S.cw + ray,
-                     make_int4(L.ci | (L.cj << 10) | (L.ck << 20), (int)L.order,
-                               (int)(((unsigned)L.fetches << 4) | (unsigned)L.oi),
-                               L.best_p));
-            LFP_STCS(S.bt + ray,
-                     L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)));
-#endif
+                        L.best_tx < 0 ? -1 : (L.best_tx | (L.best_ty << 16)),
+                        L.t_far);
         }
     }
     // queue the live rays (warp-aggregated slot allocation)
