@@ -356,12 +356,7 @@ __device__ __forceinline__ int lane_lo_step(Lane& L, const DevProbes& ps,
         if (s_out > 1.0) s_out = 1.0;
         if (lo_decide<MODE>(L.c, *L.cf, m_f, L.lo.s, s_out, L.margin, L.wx, L.wy,
                             L.wz, L.dx, L.dy, L.dz, slack, dg)) {
-            {
-                const int kq = ps.R / res;
-                const double inv_k = (kq * res == ps.R && (kq & (kq - 1)) == 0)
-                                         ? 1.0 / (double)kq : 0.0;
-                L.hi = dda_init_hi(L.c, ps.R, L.lo.s, L.lo, inv_k);
-            }
+            L.hi = dda_init_hi(L.c, ps.R, L.lo.s, L.lo, ps.inv_k);
             L.s_end = s_out;
             L.prev_s = CUDART_NAN;
             L.prev_r = 0.0;
