@@ -354,7 +354,7 @@ __device__ __forceinline__ int lane_lo_step(Lane& L, const DevProbes& ps,
     if (isfinite(m_f)) {
         double s_out = L.lo.t_max_x < L.lo.t_max_y ? L.lo.t_max_x : L.lo.t_max_y;
         if (s_out > 1.0) s_out = 1.0;
-        if (lo_decide<MODE>(L.c, *L.cf, m_f, L.lo.s, s_out, L.margin, L.wx, L.wy,
+        if (lo_decide<MODE>(ps, L.c, *L.cf, m_f, L.lo.s, s_out, L.margin, L.wx, L.wy,
                             L.wz, L.dx, L.dy, L.dz, slack, dg)) {
             L.hi = dda_init_hi(L.c, ps.R, L.lo.s, L.lo, ps.inv_k);
             L.s_end = s_out;
