@@ -215,6 +215,26 @@ class TestC5AsBenchmarked:
         np.testing.assert_allclose(res.hit_t[sel], ht, rtol=1e-4, atol=1e-6)
 
 
+    def test_page_locked_inputs_take_the_async_upload(self, c3cfg):
+        """trace_rays uploads page-locked host arrays asynchronously ahead
+        of the trace; results equal those from pageable arrays, f32 and f64,
+        and across the two record strides of the wavefront state."""
+        import torch
+        from paper_2507_14624_b200 import configs, trace_rays
+        g = c3cfg.grid
+        n = (1 << 20) + 3
+        o32, d32 = configs.c5_rays(c3cfg.scene, n)
+        ref = trace_rays(g, o32, d32)
+        po = torch.from_numpy(o32).pin_memory()
+        pd = torch.from_numpy(d32).pin_memory()
+        assert torch.from_numpy(po.numpy()).is_pinned()
+        got = trace_rays(g, po.numpy(), pd.numpy())
+        got64 = trace_rays(g, o32.astype(np.float64), d32.astype(np.float64))
+        for r in (got, got64):
+            for k in ("status", "probe", "tx", "ty", "fetch", "rgb"):
+                np.testing.assert_array_equal(getattr(r, k), getattr(ref, k), err_msg=k)
+
+
 # ---------------------------------------------------------------------------
 # The reference's acceptance setups (pkg/tests/test_acceptance.py) on the
 # CUDA path: the fixed room (scenes.py:249-270), a dense point cloud, the
