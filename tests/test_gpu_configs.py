@@ -235,6 +235,44 @@ class TestC5AsBenchmarked:
                 np.testing.assert_array_equal(getattr(r, k), getattr(ref, k), err_msg=k)
 
 
+class TestMapRatios:
+    """High-res / low-res map ratios other than the benchmarked 4: the
+    high-res DDA set-up takes its increments from the low-res DDA by exact
+    power-of-two scaling (ratios 2, 8) and falls back to one IEEE reciprocal
+    per axis otherwise (ratio 3, 6); equal maps (ratio 1)."""
+
+    @pytest.mark.parametrize("r_hi,r_lo", [(48, 16), (32, 16), (64, 8),
+                                           (48, 8), (24, 24)])
+    def test_frame_and_rays_vs_oracle(self, r_hi, r_lo):
+        from oracle import oracle
+        from paper_2507_14624_b200 import (Camera, render_frame, scenes,
+                                           trace_rays)
+        from paper_2507_14624_b200.bake import bake_grid_gpu
+        scene = scenes.room_scene(77, size=(4.0, 3.0, 4.0), n_boxes=6,
+                                  n_spheres=3)
+        g = bake_grid_gpu(scene, (0.0, 0.0, 0.0), 2.0, (3, 2, 3), r_hi, r_lo)
+        cam = Camera(eye=(1.3, 1.1, 0.9), forward=(0.5, 0.1, 0.85),
+                     vfov_deg=60.0, width=96, height=64)
+        frame = render_frame(g, cam)
+        res, _ = oracle.render_camera(g.probe_set, g.grid_origin, g.cell_size,
+                                      g.dims, cam)
+        pix, st = oracle.frame_pixels(res, cam.height, cam.width)
+        np.testing.assert_array_equal(frame.status, st)
+        np.testing.assert_array_equal(frame.pixels, pix)
+        assert abs(frame.stats["perPixelTexelFetches"] - res.fetch.mean()) < 1e-9
+        rng = np.random.default_rng(5)
+        n = 20000
+        o = rng.uniform((0.2, 0.2, 0.2), (3.8, 2.8, 3.8), (n, 3))
+        d = rng.normal(size=(n, 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        got = trace_rays(g, o, d)
+        exp = oracle.trace_rays(g.probe_set, g.grid_origin, g.cell_size, g.dims,
+                                o, d)
+        _assert_same(dict(status=got.status, probe=got.probe, tx=got.tx,
+                          ty=got.ty, fetch=got.fetch, rgb=got.rgb), exp,
+                     f"ratio {r_hi}/{r_lo}")
+
+
 # ---------------------------------------------------------------------------
 # The reference's acceptance setups (pkg/tests/test_acceptance.py) on the
 # CUDA path: the fixed room (scenes.py:249-270), a dense point cloud, the
