@@ -109,10 +109,9 @@ typedef struct {
                                    filter / by the exact path, hi-res ditto,
                                    filter-vs-exact disagreements (mode 2),
                                    low-res steps cleared by the segment
-                                   bound, hi-res texels cleared by the
-                                   squared test, segments traced, fp32-radius
-                                   path outcomes (march, occluder,
-                                   candidate)                             */
+                                   bound, (reserved, 0), segments traced,
+                                   fp32 classification outcomes (march,
+                                   occluder, candidate)                   */
     int32_t rgb_mode;
     float background[3];
     float unknown_color[3];
