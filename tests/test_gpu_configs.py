@@ -200,7 +200,11 @@ class TestC5AsBenchmarked:
         o32, d32 = configs.c5_rays(c3cfg.scene, 1 << 20)
         o_full, d_full = configs.c5_rays(c3cfg.scene, (1 << 20) + 5)
         np.testing.assert_array_equal(o32, o_full[:1 << 20])
-        res = trace_rays(g, o32, d32)     # >= 2^20 rays: wavefront schedule
+        # the schedule the bench's 2^26-ray batch takes (default from 2^22 rays)
+        res = trace_rays(g, o32, d32, schedule="wave")
+        res_p = trace_rays(g, o32, d32)   # default at this size: persistent
+        for k in ("status", "probe", "tx", "ty", "fetch", "rgb"):
+            np.testing.assert_array_equal(getattr(res_p, k), getattr(res, k), err_msg=k)
         got = dict(status=res.status, probe=res.probe, tx=res.tx, ty=res.ty,
                    fetch=res.fetch, rgb=res.rgb, hit_t=res.hit_t)
         o64, d64 = o32.astype(np.float64), d32.astype(np.float64)
@@ -224,12 +228,13 @@ class TestC5AsBenchmarked:
         g = c3cfg.grid
         n = (1 << 20) + 3
         o32, d32 = configs.c5_rays(c3cfg.scene, n)
-        ref = trace_rays(g, o32, d32)
+        ref = trace_rays(g, o32, d32, schedule="wave")
         po = torch.from_numpy(o32).pin_memory()
         pd = torch.from_numpy(d32).pin_memory()
         assert torch.from_numpy(po.numpy()).is_pinned()
-        got = trace_rays(g, po.numpy(), pd.numpy())
-        got64 = trace_rays(g, o32.astype(np.float64), d32.astype(np.float64))
+        got = trace_rays(g, po.numpy(), pd.numpy(), schedule="wave")
+        got64 = trace_rays(g, o32.astype(np.float64), d32.astype(np.float64),
+                           schedule="wave")
         for r in (got, got64):
             for k in ("status", "probe", "tx", "ty", "fetch", "rgb"):
                 np.testing.assert_array_equal(getattr(r, k), getattr(ref, k), err_msg=k)

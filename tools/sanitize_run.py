@@ -203,11 +203,11 @@ def main():
         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
     if DEBUG:
-        step("C5-like wavefront batch at 2^20 rays (default schedule)")
+        step("C5-like wavefront batch at 2^20 rays")
         o5, d5 = configs.c5_rays(c1.scene, 1 << 20, seed=3)
         t5o, t5d = torch.from_numpy(o5).cuda(), torch.from_numpy(d5).cuda()
         g = dev.grid_params(c1.grid.grid_origin, c1.grid.cell_size,
-                            c1.grid.dims, DEFAULT_CONFIG)
+                            c1.grid.dims, DEFAULT_CONFIG, schedule="wave")
         out = dev.RayOutputs(1 << 20, dps.device, probe=True, texel=True,
                              fetch=True, hit_t=True)
         c1dps = device_probe_set(c1.grid)
