@@ -303,6 +303,7 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                                           const WaveRays& rays, const WaveState& S,
                                           const int* __restrict__ q_in,
                                           long long n_in, int first,
+                                          int sparse_shift,
                                           unsigned* __restrict__ key_out,
                                           int* __restrict__ q_out,
                                           unsigned long long* __restrict__ n_out,
@@ -310,8 +311,15 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
                                           Range* rgs, EmitFn emit_fn)
 {
     const unsigned FULL = 0xffffffffu;
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = i < n_in;
+    // Small iterations (the batch's tail: a few thousand long rays) are
+    // latency-bound on the serialised paths of each warp's lanes, with most
+    // of the GPU idle: they run with 32 >> sparse_shift rays per warp, spread
+    // over more warps.
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lanes = 32 >> sparse_shift;
+    const int lane_id = threadIdx.x & 31;
+    const long long i = (t >> 5) * lanes + lane_id;
+    const bool valid = lane_id < lanes && i < n_in;
     Diag dg = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, cfs};
     dg.chs = chs;
     dg.rgs = rgs;
