@@ -61,7 +61,7 @@ typedef struct {
                                2 = filtered + re-check of every filtered
                                decision (counts into lfp_outputs.diag)    */
     int32_t schedule;       /* 0 = entry point default (cameras: nested;
-                               explicit rays: wavefront from 2^22 rays,
+                               explicit rays: wavefront from 2^21 rays,
                                persistent below); 1 = nested: one thread
                                per ray; 2 = persistent: flattened per-lane
                                state machine, lanes pull rays from a global

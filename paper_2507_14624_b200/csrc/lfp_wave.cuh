@@ -442,4 +442,74 @@ __device__ __forceinline__ void wave_step(const DevProbes& ps, const GridParams&
     emit_fn(valid && done, ray, L, dg);
 }
 
+// Tail of a batch: once few rays are left (a few thousand long ones, each
+// with dozens of probe traces to go) a wavefront iteration costs its launch,
+// sort and host round trip for almost no work. wave_finish traces each
+// remaining ray to its end in one launch: the same probe-by-probe steps
+// (K:603-647, 801-821), looped in the thread, from the ray's record.
+template <int MODE, int CFS, typename EmitFn>
+__device__ __forceinline__ void wave_finish(const DevProbes& ps, const GridParams& g,
+                                            int f32, const WaveState& S,
+                                            const int* __restrict__ q_in,
+                                            long long n_in, int sparse_shift,
+                                            ChordF* cfs, Chord* chs, Range* rgs,
+                                            EmitFn emit_fn)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lanes = 32 >> sparse_shift;
+    const int lane_id = threadIdx.x & 31;
+    const long long i = (t >> 5) * lanes + lane_id;
+    const bool valid = lane_id < lanes && i < n_in;
+    Diag dg = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, cfs};
+    dg.chs = chs;
+    dg.rgs = rgs;
+    Lane L;
+    int ray = 0;
+    if (valid) {
+        ray = LFP_LDCS(q_in + i);
+        const char* rp = wave_rec(S, ray);
+        wave_ld_ray(rp, f32, L);
+        L.steps = (L.dx > 0.0 ? 1 : 0) | (L.dy > 0.0 ? 2 : 0) | (L.dz > 0.0 ? 4 : 0);
+        double4 tm;
+        int4 cw;
+        int bt;
+        wave_ld_mut(rp, S.stride, tm, cw, bt, L.t_far);
+        wave_restore(L, g, tm, cw, bt);
+        // the range inside the current cube (K:749-756, 603-605), as the
+        // wavefront iteration forms it
+        double t_exit_cube = L.t_max_i;
+        if (L.t_max_j < t_exit_cube) t_exit_cube = L.t_max_j;
+        if (L.t_max_k < t_exit_cube) t_exit_cube = L.t_max_k;
+        if (t_exit_cube > L.t_far) t_exit_cube = L.t_far;
+        L.t0 = (0.0 > L.t_cur) ? 0.0 : L.t_cur;
+        L.t1 = t_exit_cube;
+#pragma unroll 1
+        for (;;) {
+            L.p = wave_probe(L, g);
+            const SegResult s = trace_one_probe<MODE, CFS>(
+                ps, L.p, L.ex, L.ey, L.ez, L.dx, L.dy, L.dz, L.t0, L.t1,
+                g.eps_start, g.eps_align, g.slack, dg);
+            L.fetches += s.fetches;
+            if (s.status == HIT) {
+                L.status = HIT; L.rp = L.p; L.rtx = s.tx; L.rty = s.ty;
+                break;
+            }
+            if (s.status == UNKNOWN) {
+                L.best_p = L.p; L.best_tx = s.tx; L.best_ty = s.ty;
+            }
+            L.oi++;
+            if (L.oi == 8) {
+                if (wave_next_cube(L, g)) {
+                    lane_cube(L, ps, g);   // order, oi = 0, t0 / t1 of the new cube
+                } else {
+                    L.status = MISS; L.rp = L.best_p; L.rtx = L.best_tx;
+                    L.rty = L.best_ty;
+                    break;
+                }
+            }
+        }
+    }
+    emit_fn(valid, ray, L, dg);
+}
+
 }  // namespace lfp

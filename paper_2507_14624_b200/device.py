@@ -342,7 +342,7 @@ def trace_rays(dps, gparams, origins, dirs, out, rgb_mode=1, stream=None):
 # explicit batches of at least this many rays take the wavefront schedule
 # by default (LFP_WAVE_MIN_RAYS in lfp_capi.cu); it sorts rays itself, so
 # binning them first only matters below this size
-WAVE_MIN_RAYS = 1 << 22
+WAVE_MIN_RAYS = 1 << 21
 
 
 def last_launches():

@@ -200,7 +200,7 @@ class TestC5AsBenchmarked:
         o32, d32 = configs.c5_rays(c3cfg.scene, 1 << 20)
         o_full, d_full = configs.c5_rays(c3cfg.scene, (1 << 20) + 5)
         np.testing.assert_array_equal(o32, o_full[:1 << 20])
-        # the schedule the bench's 2^26-ray batch takes (default from 2^22 rays)
+        # the schedule the bench's 2^26-ray batch takes (default from 2^21 rays)
         res = trace_rays(g, o32, d32, schedule="wave")
         res_p = trace_rays(g, o32, d32)   # default at this size: persistent
         for k in ("status", "probe", "tx", "ty", "fetch", "rgb"):
