@@ -25,4 +25,16 @@ python tools/ncu_traffic_sum.py $out/c5_traffic.csv > $out/c5_traffic.txt
 ncu --cache-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --log-file $out/c5_traffic_warm.csv python tools/c5_once.py > $out/ncu_c5tw.log 2>&1
 python tools/ncu_traffic_sum.py $out/c5_traffic_warm.csv > $out/c5_traffic_warm.txt
 rm -f $out/c5_traffic.csv $out/c5_traffic_warm.csv
-ls -la $out
+# summaries on the box (the reports together exceed gpurun's 64 MiB return)
+mkdir -p $out/summ
+for c in c1 c2 c3 c4 c5_wave; do
+  python tools/summarize_ncu.py $out/$c.ncu-rep $out/summ/r02_$c > $out/summ/${c}_dram_bytes.txt 2>&1
+done
+for c in c3 c5_wave c4 c2; do
+  ncu -i $out/$c.ncu-rep --page source --csv --print-source=cuda,sass > $out/${c}_src.csv 2>/dev/null
+  python tools/ncu_regions.py $out/${c}_src.csv > $out/summ/r02_${c}_functions.txt
+  python tools/ncu_opcodes.py $out/${c}_src.csv > $out/summ/r02_${c}_opcodes.txt
+  rm -f $out/${c}_src.csv
+done
+rm -f $out/c1.ncu-rep $out/c2.ncu-rep $out/c4.ncu-rep
+ls -la $out $out/summ
